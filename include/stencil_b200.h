@@ -1,0 +1,233 @@
+/*
+ * stencil_b200.h — C-ABI of the B200-native folded stencil sweep
+ * (arXiv 2103.09235, "Reducing Redundancy in Data Organization and Arithmetic
+ * Calculation for Stencil Computations").
+ *
+ * Citations: P:<line> = /reference PAPER.md line; S:<line> = SPEC.md line.
+ *
+ * The operation (§1): a d-dimensional grid updated iteratively in time;
+ * "the value of one point at time t is a weighted sum of itself and its
+ * neighboring points at the previous time":
+ *
+ *     u^{t+1}[p] = sum_j w_j * u^t[p + o_j]            (correlation form, the
+ *                                                       v_{i+t} index of Eq.4,
+ *                                                       P:385; R3)
+ *
+ * Temporal computation folding (§3.2-3.3, Eq.2, Eq.4-6):
+ * m time steps are applied as ONE sweep with the reassigned weights
+ * lambda^(m) = w * w * ... * w (the m-fold self-convolution of the tap map;
+ * P:335 "weights are all reassigned based on the m-step expansion").
+ *
+ * Boundary (the paper is silent — DESIGN.md reading R1): FIXED = an r-wide
+ * ring around the interior that holds u0 and is never updated.  The folded
+ * weights are not valid within (m-1)*r of a FIXED face (R2); the
+ * library evaluates that band step by step, exactly.
+ *
+ * Conventions for every entry point:
+ *  - Return value: STENCIL_OK (0) or a negative stencil_status.  Nothing
+ *    aborts or throws across this boundary.  On error, stencil_last_error()
+ *    returns a thread-local message.
+ *  - Device pointers are CUDA device pointers on the current device; they are
+ *    OWNED BY THE CALLER (PyTorch is the only allocator).  Host pointers are
+ *    plain host memory, owned by the caller.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Runs are
+ *    asynchronous on it; kernel faults surface at the caller's next
+ *    synchronisation, as with any CUDA library.
+ *  - Axes are listed slowest first (z, y, x); x has unit stride.
+ */
+#ifndef STENCIL_B200_H
+#define STENCIL_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STENCIL_MAX_DIMS 3
+#define STENCIL_MAX_FOLD 8
+
+typedef enum {
+    STENCIL_OK = 0,
+    STENCIL_EINVAL = -1,        /* bad argument (dims, radius, ncoeffs, fold_m<1, T<0, null, aliasing, misalignment) */
+    STENCIL_EUNSUPPORTED = -2,  /* valid request this build does not compile (e.g. PERIODIC on GPU, fold_m*r too large) */
+    STENCIL_ECUDA = -3,         /* CUDA runtime/driver error (message in stencil_last_error) */
+    STENCIL_ENCCL = -4,         /* NCCL error or NCCL library not loadable */
+    STENCIL_ENOMEM = -5         /* host allocation failed */
+} stencil_status;
+
+typedef enum { STENCIL_STAR = 0, STENCIL_BOX = 1 } stencil_shape;
+typedef enum { STENCIL_F32 = 0, STENCIL_F64 = 1 } stencil_dtype;
+typedef enum { STENCIL_BC_FIXED = 0, STENCIL_BC_PERIODIC = 1 } stencil_boundary;
+
+typedef struct stencil_plan_s *stencil_plan;
+typedef struct stencil_comm_s *stencil_comm;
+
+/*
+ * Buffer layout the library requires.  The caller allocates
+ * `bytes` bytes (device, >= 256-byte aligned as cudaMalloc/PyTorch give) and
+ * addresses interior point (i_0, .., i_{d-1}) at element index
+ *     sum_a (origin[a] + i_a) * stride[a].
+ * The physical ring occupies interior coordinates [-r, 0) and [N_a, N_a + r)
+ * on every axis.  The unit-stride axis has a left pad so interior x = 0 is
+ * 128-byte aligned, and its row pitch (stride of the next axis) is a multiple
+ * of 128 bytes (TMA needs 16-byte multiples).  Pad cells outside the ring are
+ * never used for any result.  For dist layouts (stencil_plan_layout_dist)
+ * axis 0 carries `halo` ghost planes on each side instead of the ring; at the
+ * global ends the r planes next to the interior are the physical ring.
+ */
+typedef struct {
+    int ndim;
+    int radius;               /* r */
+    int64_t interior[STENCIL_MAX_DIMS]; /* N_a (local N for dist layouts) */
+    int64_t extent[STENCIL_MAX_DIMS];   /* allocated extent per axis (elements) */
+    int64_t stride[STENCIL_MAX_DIMS];   /* element stride per axis */
+    int64_t origin[STENCIL_MAX_DIMS];   /* index of interior coordinate 0 per axis */
+    int64_t elem_bytes;       /* 4 (F32) or 8 (F64) */
+    int64_t bytes;            /* allocation size */
+    int64_t global_offset0;   /* dist: global interior index of local plane 0 on axis 0 (else 0) */
+} stencil_layout;
+
+/*
+ * Create a plan (host only; no CUDA call).
+ *   ndim     1..3; dims[ndim] interior extents, slowest first, each >= 1.
+ *   radius   r >= 1.
+ *   shape    STAR: taps = offsets in [-r,r]^d with at most one nonzero
+ *            coordinate (k = 2dr+1); BOX: all of [-r,r]^d (k = (2r+1)^d)
+ *            (SPEC.md:31-32).
+ *   coeffs   ncoeffs == k fp64 weights in CANONICAL tap order: offsets in
+ *            lexicographic order, slowest axis outermost, each axis -r..r
+ *            (R4).  Copied.
+ *   dtype    storage + arithmetic type on the GPU.  Folded weights are computed
+ *            in fp64 and rounded once to dtype.
+ *   boundary FIXED (supported on GPU) or PERIODIC (EUNSUPPORTED at run time).
+ * Errors: EINVAL on any bad argument.
+ */
+int stencil_plan_create(stencil_plan *plan, int ndim, const int64_t *dims, int radius,
+                        stencil_shape shape, const double *coeffs, int ncoeffs,
+                        stencil_dtype dtype, stencil_boundary boundary);
+int stencil_plan_destroy(stencil_plan plan);
+
+/* Single-GPU buffer layout (for `in`, `out` and the workspace). */
+int stencil_plan_layout(stencil_plan plan, stencil_layout *out);
+
+/* Number of taps k, and the canonical offsets (k * ndim ints, slowest first). */
+int stencil_plan_ntaps(stencil_plan plan, int *ntaps);
+int stencil_plan_taps(stencil_plan plan, int *offsets, int cap);
+
+/*
+ * The library's folding matrix lambda^(m) (Eq.2; the counterpart rows
+ * of Eq.4-6) as a dense (2mr+1)^ndim fp64 array, index [o + m r],
+ * slowest axis first.  Host only.  cap = capacity in doubles.
+ * Errors: EINVAL if m < 1 or cap too small; EUNSUPPORTED if m > STENCIL_MAX_FOLD.
+ */
+int stencil_plan_fold_coeffs(stencil_plan plan, int m, double *dense, int64_t cap);
+
+/* Workspace bytes stencil_run needs (one more buffer of the plan's layout). */
+int stencil_workspace_size(stencil_plan plan, int64_t *bytes);
+
+/*
+ * K-G0: fill a device buffer (plan layout) with the seeded input field
+ * u0 = U(seed, i), i = row-major index of the point in the UNALIGNED padded
+ * frame prod(N_a + 2r) (R6), over the interior and the ring.  Pads
+ * are set to 0.  Async on stream.
+ */
+int stencil_fill_random(stencil_plan plan, void *buf, uint64_t seed, void *stream);
+
+/*
+ * Run T time steps: out = S^T(in), with fold_m steps per sweep (Eq.2):
+ *   floor(T / fold_m) folded sweeps, then T mod fold_m single steps
+ *   (R10).  Jacobi ping-pong between `out` and `workspace`
+ *    arranged so the last sweep writes `out`; `in` is never written.
+ *   T = 0 copies in -> out.  Every sweep = the folded interior sweep plus the
+ *   stepwise band within (fold_m-1)*r of each face.
+ * in, out, workspace: device buffers of the plan layout (workspace may be NULL
+ *   when at most one sweep runs).  `out` is fully written, ring included.
+ * Errors: EINVAL (T < 0, fold_m < 1, null/aliased/misaligned pointers),
+ *   EUNSUPPORTED (PERIODIC; fold_m*r > STENCIL_MAX_FOLD), ECUDA.
+ */
+int stencil_run(stencil_plan plan, const void *in, void *out, int64_t T, int fold_m,
+                void *workspace, void *stream);
+
+/*
+ * As stencil_run, selecting the on-chip evaluation of each m-step sweep:
+ *   stages = 1 : the folded sweep (one pass of lambda^(m), §3.3);
+ *   stages = m : the on-chip m-step temporal block (m single steps per tile,
+ *                "time loop fusion");
+ *   1 < stages < m, stages | m : stages on-chip passes of lambda^(m/stages);
+ *   stages = 0 : the plan's choice (FMA-vs-byte budget).
+ * Results are identical up to fp rounding for every choice.
+ */
+int stencil_run_ex(stencil_plan plan, const void *in, void *out, int64_t T, int fold_m,
+                   int stages, void *workspace, void *stream);
+
+/*
+ * End-to-end call with HOST buffers (for the e2e measurement): copies
+ * in_host (plan layout, pinned recommended) -> dev_in, runs stencil_run_ex,
+ * copies dev_out -> out_host, all enqueued on `stream`.  Does not synchronise.
+ */
+int stencil_run_host(stencil_plan plan, const void *in_host, void *out_host, int64_t T,
+                     int fold_m, int stages, void *dev_in, void *dev_out, void *workspace,
+                     void *stream);
+
+/* Number of kernel launches the last run on this plan enqueued (host count). */
+int stencil_plan_last_launches(stencil_plan plan, int64_t *launches);
+
+/* ---------------------------------------------------------------- multi-GPU
+ * Slab decomposition along axis 0 (the slowest axis), one process per GPU
+ * (SURVEY §8(e)).  Rank g owns interior planes [g*N0/G, (g+1)*N0/G) plus
+ * `halo` ghost planes per side (halo >= fold_m * r for every run).  Per sweep
+ * the first/last fold_m*r local planes are computed first and exchanged with
+ * rank g-1 / g+1 (grouped ncclSend/ncclRecv on a comm stream) while the rest
+ * of the slab is computed.  Slab seams are not physical faces: no band there.
+ */
+
+/* 128-byte NCCL unique id (rank 0 creates, caller broadcasts). */
+int stencil_comm_unique_id(unsigned char id[128]);
+/* Create a communicator on the current CUDA device. */
+int stencil_comm_create(stencil_comm *comm, const unsigned char id[128], int rank, int nranks);
+int stencil_comm_destroy(stencil_comm comm);
+
+/* Local layout of rank `rank` of `nranks` with `halo` ghost planes.
+ * EINVAL if N0 is not divisible by nranks or a slab is thinner than halo. */
+int stencil_plan_layout_dist(stencil_plan plan, int rank, int nranks, int halo,
+                             stencil_layout *out);
+
+/* K-G0 for a local slab: the same global field, ghost planes included. */
+int stencil_fill_random_dist(stencil_plan plan, int rank, int nranks, int halo, void *buf,
+                             uint64_t seed, void *stream);
+
+/*
+ * Distributed run.  in_local / out_local / workspace: local slab buffers
+ * (stencil_plan_layout_dist with the same halo).  in_local's ghost planes must
+ * hold the neighbours' planes (stencil_fill_random_dist provides that, or call
+ * stencil_halo_exchange first).  All ranks call collectively.
+ */
+int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void *in_local,
+                     void *out_local, int64_t T, int fold_m, int stages, int halo,
+                     void *workspace, void *stream);
+
+/* Exchange the ghost planes of a local slab buffer (collective). */
+int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void *buf, int halo,
+                          void *stream);
+
+/*
+ * The same distributed algorithm with all `nranks` ranks in THIS process on
+ * the current device, exchanging ghost planes with device-to-device copies
+ * instead of NCCL (identical kernels, boxes and ordering; used by tests on
+ * one GPU).  Arrays of nranks pointers.
+ */
+int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void *const *in_locals,
+                              void *const *out_locals, int64_t T, int fold_m, int stages,
+                              int halo, void *const *workspaces, void *stream);
+
+/* Thread-local message for the last error on this thread ("" if none). */
+const char *stencil_last_error(void);
+
+/* Library version string. */
+const char *stencil_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STENCIL_B200_H */

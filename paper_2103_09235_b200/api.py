@@ -1,0 +1,221 @@
+"""Thin Python binding over the C-ABI (argument marshalling only).
+
+Every step of the path runs in the library's CUDA kernels; PyTorch supplies
+device memory, streams and (for multi-GPU) process groups.
+
+    plan = Plan(dims=(8192, 8192), radius=1, shape="star", coeffs=w, dtype="f64")
+    a, b, ws = plan.empty(), plan.empty(), plan.empty()
+    plan.fill_random(a, seed=2)
+    plan.run(a, b, T=200, fold_m=2, workspace=ws)
+    u = plan.frame_view(b)          # strided view of the padded frame (N + 2r per axis)
+"""
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+import torch
+
+from ._lib import StencilLayout, check, load
+
+STAR, BOX = 0, 1
+F32, F64 = 0, 1
+FIXED, PERIODIC = 0, 1
+_SHAPES = {"star": STAR, "box": BOX, STAR: STAR, BOX: BOX}
+_DTYPES = {"f32": F32, "fp32": F32, "float32": F32, torch.float32: F32,
+           "f64": F64, "fp64": F64, "float64": F64, torch.float64: F64, F32: F32, F64: F64}
+_BCS = {"fixed": FIXED, "periodic": PERIODIC, FIXED: FIXED, PERIODIC: PERIODIC}
+
+
+@dataclass(frozen=True)
+class Layout:
+    ndim: int
+    radius: int
+    interior: tuple
+    extent: tuple
+    stride: tuple
+    origin: tuple
+    elem_bytes: int
+    bytes: int
+    global_offset0: int
+
+    @property
+    def numel(self) -> int:
+        return self.bytes // self.elem_bytes
+
+    @property
+    def frame(self) -> tuple:
+        """Padded-frame extents N_a + 2r (axis 0 of a dist layout: local N + 2r)."""
+        return tuple(n + 2 * self.radius for n in self.interior)
+
+
+def _layout(cl: StencilLayout) -> Layout:
+    nd = cl.ndim
+    return Layout(nd, cl.radius, tuple(cl.interior[:nd]), tuple(cl.extent[:nd]), tuple(cl.stride[:nd]),
+                  tuple(cl.origin[:nd]), cl.elem_bytes, cl.bytes, cl.global_offset0)
+
+
+def _ptr(t) -> Optional[int]:
+    if t is None:
+        return None
+    if isinstance(t, torch.Tensor):
+        return t.data_ptr()
+    return int(t)
+
+
+def _stream(stream) -> Optional[int]:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    if isinstance(stream, torch.cuda.Stream):
+        return stream.cuda_stream
+    return int(stream)
+
+
+class Plan:
+    """stencil_plan_create(dims, radius, shape, coeffs, dtype, boundary)."""
+
+    def __init__(self, dims: Sequence[int], radius: int, shape, coeffs, dtype="f64", boundary="fixed"):
+        self._lib = load()
+        self.dims = tuple(int(d) for d in dims)
+        self.ndim = len(self.dims)
+        self.radius = int(radius)
+        self.shape = _SHAPES[shape]
+        self.dtype_code = _DTYPES[dtype]
+        self.torch_dtype = torch.float64 if self.dtype_code == F64 else torch.float32
+        self.boundary = _BCS[boundary]
+        w = np.ascontiguousarray(coeffs, dtype=np.float64)
+        self.coeffs = w.copy()
+        h = ctypes.c_void_p()
+        d = (ctypes.c_int64 * self.ndim)(*self.dims)
+        check(self._lib.stencil_plan_create(ctypes.byref(h), self.ndim, d, self.radius, self.shape,
+                                            w.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), len(w),
+                                            self.dtype_code, self.boundary))
+        self._h = h
+        cl = StencilLayout()
+        check(self._lib.stencil_plan_layout(self._h, ctypes.byref(cl)))
+        self.layout = _layout(cl)
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value:
+            self._lib.stencil_plan_destroy(h)
+            self._h = None
+
+    # ---------------------------------------------------------------- host info
+    @property
+    def ntaps(self) -> int:
+        k = ctypes.c_int()
+        check(self._lib.stencil_plan_ntaps(self._h, ctypes.byref(k)))
+        return k.value
+
+    def taps(self):
+        k = self.ntaps
+        buf = (ctypes.c_int * (k * self.ndim))()
+        check(self._lib.stencil_plan_taps(self._h, buf, k * self.ndim))
+        return [tuple(buf[j * self.ndim:(j + 1) * self.ndim]) for j in range(k)]
+
+    def fold_coeffs(self, m: int) -> np.ndarray:
+        """lambda^(m) as a dense (2mr+1)^d fp64 array (index o + m r)."""
+        side = 2 * m * self.radius + 1
+        out = np.zeros((side,) * self.ndim, dtype=np.float64)
+        check(self._lib.stencil_plan_fold_coeffs(self._h, int(m), out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                                 out.size))
+        return out
+
+    def layout_dist(self, rank: int, nranks: int, halo: int) -> Layout:
+        cl = StencilLayout()
+        check(self._lib.stencil_plan_layout_dist(self._h, rank, nranks, halo, ctypes.byref(cl)))
+        return _layout(cl)
+
+    # ---------------------------------------------------------------- buffers
+    def empty(self, device="cuda", layout: Optional[Layout] = None, pin_memory=False) -> torch.Tensor:
+        L = layout or self.layout
+        if device == "cpu":
+            return torch.zeros(L.numel, dtype=self.torch_dtype, pin_memory=pin_memory)
+        return torch.empty(L.numel, dtype=self.torch_dtype, device=device)
+
+    def frame_view(self, buf: torch.Tensor, layout: Optional[Layout] = None) -> torch.Tensor:
+        """Strided view of the padded frame (interior + r-ring) of a buffer."""
+        L = layout or self.layout
+        r = L.radius
+        off = sum((L.origin[a] - r) * L.stride[a] for a in range(L.ndim))
+        return buf.as_strided(L.frame, L.stride, buf.storage_offset() + off)
+
+    def interior_view(self, buf: torch.Tensor, layout: Optional[Layout] = None) -> torch.Tensor:
+        L = layout or self.layout
+        off = sum(L.origin[a] * L.stride[a] for a in range(L.ndim))
+        return buf.as_strided(L.interior, L.stride, buf.storage_offset() + off)
+
+    def from_frame(self, frame: np.ndarray, device="cuda") -> torch.Tensor:
+        """A buffer in the plan layout holding `frame` (padded frame array); pads = 0."""
+        buf = torch.zeros(self.layout.numel, dtype=self.torch_dtype)
+        self.frame_view(buf).copy_(torch.from_numpy(np.asarray(frame, dtype=np.float64)).to(self.torch_dtype))
+        return buf.to(device) if device != "cpu" else buf
+
+    # ---------------------------------------------------------------- compute
+    def fill_random(self, buf: torch.Tensor, seed: int, stream=None):
+        check(self._lib.stencil_fill_random(self._h, _ptr(buf), int(seed), _stream(stream)))
+
+    def run(self, inp, out, T: int, fold_m: int = 1, workspace=None, stages: int = 0, stream=None):
+        check(self._lib.stencil_run_ex(self._h, _ptr(inp), _ptr(out), int(T), int(fold_m), int(stages),
+                                       _ptr(workspace), _stream(stream)))
+
+    def run_host(self, in_host, out_host, T: int, fold_m: int, dev_in, dev_out, workspace=None, stages: int = 0,
+                 stream=None):
+        check(self._lib.stencil_run_host(self._h, _ptr(in_host), _ptr(out_host), int(T), int(fold_m), int(stages),
+                                         _ptr(dev_in), _ptr(dev_out), _ptr(workspace), _stream(stream)))
+
+    @property
+    def last_launches(self) -> int:
+        n = ctypes.c_int64()
+        check(self._lib.stencil_plan_last_launches(self._h, ctypes.byref(n)))
+        return n.value
+
+    # ---------------------------------------------------------------- multi-GPU
+    def fill_random_dist(self, rank, nranks, halo, buf, seed, stream=None):
+        check(self._lib.stencil_fill_random_dist(self._h, rank, nranks, halo, _ptr(buf), int(seed), _stream(stream)))
+
+    def run_dist(self, comm: "Comm", inp, out, T, fold_m, halo, workspace=None, stages=0, stream=None):
+        check(self._lib.stencil_run_dist(self._h, comm._h, _ptr(inp), _ptr(out), int(T), int(fold_m), int(stages),
+                                         int(halo), _ptr(workspace), _stream(stream)))
+
+    def halo_exchange(self, comm: "Comm", buf, halo, stream=None):
+        check(self._lib.stencil_halo_exchange(self._h, comm._h, _ptr(buf), int(halo), _stream(stream)))
+
+    def run_dist_emulated(self, ins, outs, T, fold_m, halo, workspaces=None, stages=0, stream=None):
+        n = len(ins)
+        arr = ctypes.c_void_p * n
+        wp = arr(*[_ptr(w) for w in workspaces]) if workspaces is not None else None
+        check(self._lib.stencil_run_dist_emulated(self._h, n, arr(*[_ptr(t) for t in ins]),
+                                                  arr(*[_ptr(t) for t in outs]), int(T), int(fold_m), int(stages),
+                                                  int(halo), wp, _stream(stream)))
+
+
+class Comm:
+    """NCCL communicator over the slab decomposition (one process per GPU).
+
+    Bootstrap: rank 0 creates the 128-byte unique id, which is broadcast through
+    torch.distributed (see paper_2103_09235_b200.dist.make_comm)."""
+
+    def __init__(self, uid: bytes, rank: int, nranks: int):
+        self._lib = load()
+        h = ctypes.c_void_p()
+        check(self._lib.stencil_comm_create(ctypes.byref(h), uid, int(rank), int(nranks)))
+        self._h = h
+        self.rank, self.nranks = rank, nranks
+
+    @staticmethod
+    def unique_id() -> bytes:
+        buf = ctypes.create_string_buffer(128)
+        check(load().stencil_comm_unique_id(buf))
+        return buf.raw
+
+    def close(self):
+        if getattr(self, "_h", None) is not None and self._h.value:
+            self._lib.stencil_comm_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()

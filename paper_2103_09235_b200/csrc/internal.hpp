@@ -1,0 +1,116 @@
+// internal.hpp — host-side structures of the B200 stencil library (not part
+// of the C-ABI).  See include/stencil_b200.h for the contract and DESIGN.md
+// for the design.
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+#include <map>
+#include <mutex>
+
+#include "../../include/stencil_b200.h"
+
+namespace sb {
+
+// ------------------------------------------------------------------ errors
+int set_error(int code, const std::string& msg);
+int cuda_error(int cuda_err, const char* what);
+
+// ------------------------------------------------------------------ geometry
+// Everything is kept as 3 axes internally: axis 0 = streaming axis (z in 3D,
+// y in 2D, unused in 1D), axis 1 = y (3D only), axis 2 = x (unit stride).
+struct Box {
+    int64_t lo[3], hi[3];   // interior coordinates, half-open
+    bool empty() const { return lo[0] >= hi[0] || lo[1] >= hi[1] || lo[2] >= hi[2]; }
+    int64_t volume() const { return empty() ? 0 : (hi[0] - lo[0]) * (hi[1] - lo[1]) * (hi[2] - lo[2]); }
+};
+
+struct Layout3 {
+    int ndim = 0;
+    int r = 1;
+    int64_t n[3] = {1, 1, 1};        // local interior extents
+    int64_t ext[3] = {1, 1, 1};      // allocated extents
+    int64_t stride[3] = {0, 0, 1};   // element strides
+    int64_t origin[3] = {0, 0, 0};   // allocation index of interior 0
+    int64_t lo_valid[3] = {0, 0, 0}; // cells below 0 that hold data (r, or halo for ghosts)
+    int64_t hi_valid[3] = {0, 0, 0};
+    int phys_lo[3] = {1, 1, 1};      // 1 = physical (frozen-ring) face
+    int phys_hi[3] = {1, 1, 1};
+    int64_t esize = 8;
+    int64_t bytes = 0;
+    int64_t gofs0 = 0;               // dist: global index of local plane 0
+    int64_t gn[3] = {1, 1, 1};       // global interior extents
+};
+
+// ------------------------------------------------------------------ plan
+struct Plan {
+    int ndim;
+    int64_t dims[3];     // user order, slowest first
+    int r;
+    int shape;           // STENCIL_STAR / STENCIL_BOX
+    int dtype;           // STENCIL_F32 / STENCIL_F64
+    int boundary;
+    std::vector<int> taps;       // k * ndim canonical offsets
+    std::vector<double> w;       // k weights (fp64)
+    // folded maps lambda^(q) as dense (2qr+1)^ndim fp64, q = 1..STENCIL_MAX_FOLD
+    std::map<int, std::vector<double>> lam;
+    std::mutex mu;
+    int64_t last_launches = 0;
+    int sm_count = 0;
+    int device = -1;
+};
+
+const std::vector<double>& folded(Plan* p, int q);   // cached lambda^(q)
+Layout3 make_layout(const Plan* p, int rank, int nranks, int halo);
+void to_public(const Layout3& L, stencil_layout* out);
+
+// Evaluation variant of one m-step sweep on the main (folded-valid) region.
+struct Variant { int q; int stages; };
+Variant choose_variant(const Plan* p, int m);
+int support_size(int ndim, int shape, int r, int q);
+
+// ------------------------------------------------------------------ kernels
+// Sweep of the main region with `stages` on-chip passes of lambda^(q).
+// Returns number of launches (>=0) or a negative status.
+struct SweepCall {
+    const void* src;
+    void* dst;
+    const Layout3* L;
+    std::vector<Box> boxes;   // output boxes (interior coords)
+    int q, stages;
+    const std::vector<double>* coef;   // lambda^(q), dense fp64
+    void* stream;
+};
+int launch_sweep(Plan* p, const SweepCall& c);
+
+// Exact stepwise m-step band over boxes (K-G3).
+struct BandCall {
+    const void* src;
+    void* dst;
+    const Layout3* L;
+    std::vector<Box> boxes;
+    int m;
+    void* stream;
+};
+int launch_band(Plan* p, const BandCall& c);
+
+// 1D on-chip multi-step kernel (K-G4): T steps (fold m) in one launch.
+int launch_1d(Plan* p, const void* src, void* dst, const Layout3* L, int64_t T, int m,
+              int stages_flag, void* stream);
+
+// Copy every non-interior cell (ring, ghosts, pads) src -> dst (K-G5).
+int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void* stream);
+// K-G0 seeded field over the frame (global padded index).
+int launch_fill(Plan* p, void* buf, const Layout3* L, uint64_t seed, void* stream);
+
+// ------------------------------------------------------------------ run
+int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages, void* ws,
+               void* stream);
+
+struct Transport {
+    virtual ~Transport() {}
+    // Exchange: for every rank, send planes [lo,hi) of `bufs[rank]` to the
+    // neighbour's ghost planes. Implementation-specific.
+};
+
+}  // namespace sb

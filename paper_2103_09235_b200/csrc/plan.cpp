@@ -1,0 +1,335 @@
+// plan.cpp — plan creation, canonical taps, the coefficient-folding generator
+// (SURVEY §8(a) a1/a2), buffer layouts and the evaluation-variant choice.
+// Host only: nothing here calls CUDA.
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <new>
+
+#include "internal.hpp"
+
+namespace sb {
+
+static thread_local std::string g_err;
+
+int set_error(int code, const std::string& msg) {
+    g_err = msg;
+    return code;
+}
+
+static int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+// Canonical taps (R4): offsets in [-r, r]^d, lexicographic with the
+// slowest axis outermost; STAR keeps offsets with at most one nonzero
+// coordinate.
+static std::vector<int> canonical_taps(int nd, int r, int shape) {
+    std::vector<int> out;
+    int o[3];
+    int side = 2 * r + 1;
+    int total = 1;
+    for (int a = 0; a < nd; ++a) total *= side;
+    for (int idx = 0; idx < total; ++idx) {
+        int t = idx, nz = 0;
+        for (int a = nd - 1; a >= 0; --a) {
+            o[a] = t % side - r;
+            t /= side;
+            nz += o[a] != 0;
+        }
+        if (shape == STENCIL_STAR && nz > 1) continue;
+        for (int a = 0; a < nd; ++a) out.push_back(o[a]);
+    }
+    return out;
+}
+
+// ---------------------------------------------------------------- folding
+// lambda^(q) (Eq.2) by binary powering of sparse offset maps:
+// lambda^(a+b) = lambda^(a) (*) lambda^(b) (the semigroup property),
+// with (*) the convolution of coefficient maps (offsets add — composing two
+// correlations, R3).  Independent of the oracle's repeated dense
+// convolution; tests compare the two.
+using Key = std::array<int, 3>;
+using SparseMap = std::map<Key, double>;
+
+static SparseMap sparse_conv(const SparseMap& a, const SparseMap& b) {
+    SparseMap out;
+    for (const auto& ea : a)
+        for (const auto& eb : b) {
+            Key k = {ea.first[0] + eb.first[0], ea.first[1] + eb.first[1], ea.first[2] + eb.first[2]};
+            out[k] += ea.second * eb.second;
+        }
+    return out;
+}
+
+static SparseMap fold_sparse(const Plan* p, int q) {
+    SparseMap base;
+    int nd = p->ndim;
+    for (size_t j = 0; j < p->w.size(); ++j) {
+        Key k = {0, 0, 0};
+        for (int a = 0; a < nd; ++a) k[a] = p->taps[j * nd + a];
+        base[k] += p->w[j];
+    }
+    SparseMap result;
+    bool have = false;
+    SparseMap pw = base;
+    int e = q;
+    while (e > 0) {
+        if (e & 1) {
+            result = have ? sparse_conv(result, pw) : pw;
+            have = true;
+        }
+        e >>= 1;
+        if (e) pw = sparse_conv(pw, pw);
+    }
+    return result;
+}
+
+const std::vector<double>& folded(Plan* p, int q) {
+    std::lock_guard<std::mutex> g(p->mu);
+    auto it = p->lam.find(q);
+    if (it != p->lam.end()) return it->second;
+    SparseMap sm = fold_sparse(p, q);
+    int nd = p->ndim, R = q * p->r, side = 2 * R + 1;
+    int64_t total = 1;
+    for (int a = 0; a < nd; ++a) total *= side;
+    std::vector<double> dense((size_t)total, 0.0);
+    for (const auto& e : sm) {
+        int64_t idx = 0;
+        for (int a = 0; a < nd; ++a) idx = idx * side + (e.first[a] + R);
+        dense[(size_t)idx] = e.second;
+    }
+    return p->lam.emplace(q, std::move(dense)).first->second;
+}
+
+int support_size(int nd, int shape, int r, int q) {
+    int R = q * r, side = 2 * R + 1, cnt = 0, total = 1;
+    for (int a = 0; a < nd; ++a) total *= side;
+    for (int idx = 0; idx < total; ++idx) {
+        int t = idx, s = 0;
+        bool ok = true;
+        for (int a = 0; a < nd; ++a) {
+            int o = t % side - R;
+            t /= side;
+            s += (std::abs(o) + r - 1) / r;
+        }
+        if (shape == STENCIL_STAR) ok = s <= q;
+        cnt += ok;
+    }
+    return cnt;
+}
+
+// ---------------------------------------------------------------- variants
+// FMA-vs-byte budget (the GPU form of the paper's
+// profitability index Eq.3): a sweep streams 2*sizeof(T) bytes per point, so at
+// the HBM roofline it can afford about `budget` FMAs per point.  Prefer the
+// fully folded pass (fewest passes); otherwise the divisor split with the
+// fewest FMAs (stages * |supp lambda^(q)|, plus the overlapped-tile halo).
+Variant choose_variant(const Plan* p, int m) {
+    if (m <= 1) return {1, 1};
+    double budget = p->dtype == STENCIL_F64 ? 28.0 : 56.0;
+    int full = support_size(p->ndim, p->shape, p->r, m);
+    if (full <= budget) return {m, 1};
+    Variant best = {m, 1};
+    double best_cost = 1e30;
+    for (int s = 1; s <= m; ++s) {
+        if (m % s) continue;
+        int q = m / s;
+        double red = 1.0;
+        if (s > 1) {
+            double w = p->ndim == 3 ? 16.0 : 256.0;
+            red = (w + 2.0 * (s - 1) * q * p->r) / w;
+            if (p->ndim == 3) red *= (64.0 + 2.0 * (s - 1) * q * p->r) / 64.0;
+        }
+        double cost = s * support_size(p->ndim, p->shape, p->r, q) * red;
+        if (cost < best_cost) { best_cost = cost; best = {q, s}; }
+    }
+    return best;
+}
+
+// ---------------------------------------------------------------- layouts
+// SURVEY §8(b) Layout: ring of r cells on every axis; the unit-stride axis has
+// a left pad so interior x = 0 is 128-byte aligned and a pitch that is a
+// multiple of 128 bytes.  Dist: axis 0 carries `halo` ghost planes per side.
+Layout3 make_layout(const Plan* p, int rank, int nranks, int halo) {
+    Layout3 L;
+    L.ndim = p->ndim;
+    L.r = p->r;
+    L.esize = p->dtype == STENCIL_F64 ? 8 : 4;
+    int64_t al = 128 / L.esize;
+    int nd = p->ndim;
+    // map user axes (slowest first) -> internal axes (0 stream, 1 y, 2 x)
+    int64_t g[3] = {1, 1, 1};
+    if (nd == 1) g[2] = p->dims[0];
+    if (nd == 2) { g[0] = p->dims[0]; g[2] = p->dims[1]; }
+    if (nd == 3) { g[0] = p->dims[0]; g[1] = p->dims[1]; g[2] = p->dims[2]; }
+    for (int a = 0; a < 3; ++a) { L.gn[a] = g[a]; L.n[a] = g[a]; }
+    bool used[3] = {nd >= 2, nd == 3, true};
+    for (int a = 0; a < 3; ++a) {
+        if (!used[a]) {
+            L.phys_lo[a] = L.phys_hi[a] = 0;
+            L.lo_valid[a] = L.hi_valid[a] = 0;
+        } else {
+            L.lo_valid[a] = L.hi_valid[a] = p->r;
+        }
+    }
+    // x
+    L.origin[2] = round_up(p->r, al);
+    L.ext[2] = round_up(L.origin[2] + g[2] + p->r, al);
+    L.stride[2] = 1;
+    // y
+    if (used[1]) { L.origin[1] = p->r; L.ext[1] = g[1] + 2 * p->r; }
+    else { L.origin[1] = 0; L.ext[1] = 1; }
+    L.stride[1] = L.ext[2];
+    // stream axis
+    if (used[0]) {
+        int64_t nloc = g[0] / nranks;
+        L.n[0] = nloc;
+        L.gofs0 = nloc * rank;
+        int64_t h = nranks > 1 ? halo : p->r;
+        if (h < p->r) h = p->r;
+        L.origin[0] = h;
+        L.ext[0] = nloc + 2 * h;
+        L.phys_lo[0] = rank == 0;
+        L.phys_hi[0] = rank == nranks - 1;
+        L.lo_valid[0] = L.phys_lo[0] ? p->r : h;
+        L.hi_valid[0] = L.phys_hi[0] ? p->r : h;
+    } else {
+        L.origin[0] = 0;
+        L.ext[0] = 1;
+    }
+    L.stride[0] = L.ext[1] * L.stride[1];
+    L.bytes = L.ext[0] * L.stride[0] * L.esize;
+    return L;
+}
+
+void to_public(const Layout3& L, stencil_layout* out) {
+    std::memset(out, 0, sizeof(*out));
+    out->ndim = L.ndim;
+    out->radius = L.r;
+    int map[3];
+    if (L.ndim == 1) { map[0] = 2; }
+    if (L.ndim == 2) { map[0] = 0; map[1] = 2; }
+    if (L.ndim == 3) { map[0] = 0; map[1] = 1; map[2] = 2; }
+    for (int a = 0; a < L.ndim; ++a) {
+        int i = map[a];
+        out->interior[a] = L.n[i];
+        out->extent[a] = L.ext[i];
+        out->stride[a] = L.stride[i];
+        out->origin[a] = L.origin[i];
+    }
+    out->elem_bytes = L.esize;
+    out->bytes = L.bytes;
+    out->global_offset0 = L.gofs0;
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+const char* stencil_last_error(void) { return g_err.c_str(); }
+
+const char* stencil_version(void) { return "paper_2103_09235_b200 0.1 (sm_100a)"; }
+
+int stencil_plan_create(stencil_plan* plan, int ndim, const int64_t* dims, int radius,
+                        stencil_shape shape, const double* coeffs, int ncoeffs,
+                        stencil_dtype dtype, stencil_boundary boundary) {
+    g_err.clear();
+    if (!plan) return set_error(STENCIL_EINVAL, "plan pointer is NULL");
+    *plan = nullptr;
+    if (ndim < 1 || ndim > 3) return set_error(STENCIL_EINVAL, "ndim must be 1..3");
+    if (!dims) return set_error(STENCIL_EINVAL, "dims is NULL");
+    for (int a = 0; a < ndim; ++a)
+        if (dims[a] < 1 || dims[a] > (int64_t(1) << 31))
+            return set_error(STENCIL_EINVAL, "every interior extent must be in [1, 2^31]");
+    if (radius < 1 || radius > 4) return set_error(STENCIL_EINVAL, "radius must be 1..4");
+    if (shape != STENCIL_STAR && shape != STENCIL_BOX) return set_error(STENCIL_EINVAL, "bad shape");
+    if (dtype != STENCIL_F32 && dtype != STENCIL_F64) return set_error(STENCIL_EINVAL, "bad dtype");
+    if (boundary != STENCIL_BC_FIXED && boundary != STENCIL_BC_PERIODIC)
+        return set_error(STENCIL_EINVAL, "bad boundary");
+    std::vector<int> taps = canonical_taps(ndim, radius, shape);
+    int k = (int)taps.size() / ndim;
+    if (!coeffs || ncoeffs != k)
+        return set_error(STENCIL_EINVAL, "ncoeffs must equal the canonical tap count " + std::to_string(k));
+    for (int j = 0; j < k; ++j)
+        if (!std::isfinite(coeffs[j])) return set_error(STENCIL_EINVAL, "coefficients must be finite");
+    Plan* p = new (std::nothrow) Plan();
+    if (!p) return set_error(STENCIL_ENOMEM, "out of host memory");
+    p->ndim = ndim;
+    for (int a = 0; a < 3; ++a) p->dims[a] = a < ndim ? dims[a] : 1;
+    p->r = radius;
+    p->shape = shape;
+    p->dtype = dtype;
+    p->boundary = boundary;
+    p->taps = taps;
+    p->w.assign(coeffs, coeffs + k);
+    *plan = reinterpret_cast<stencil_plan>(p);
+    return STENCIL_OK;
+}
+
+int stencil_plan_destroy(stencil_plan plan) {
+    delete reinterpret_cast<Plan*>(plan);
+    return STENCIL_OK;
+}
+
+int stencil_plan_layout(stencil_plan plan, stencil_layout* out) {
+    if (!plan || !out) return set_error(STENCIL_EINVAL, "NULL argument");
+    to_public(make_layout(reinterpret_cast<Plan*>(plan), 0, 1, 0), out);
+    return STENCIL_OK;
+}
+
+int stencil_plan_ntaps(stencil_plan plan, int* ntaps) {
+    if (!plan || !ntaps) return set_error(STENCIL_EINVAL, "NULL argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    *ntaps = (int)p->w.size();
+    return STENCIL_OK;
+}
+
+int stencil_plan_taps(stencil_plan plan, int* offsets, int cap) {
+    if (!plan || !offsets) return set_error(STENCIL_EINVAL, "NULL argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (cap < (int)p->taps.size()) return set_error(STENCIL_EINVAL, "capacity too small");
+    std::copy(p->taps.begin(), p->taps.end(), offsets);
+    return STENCIL_OK;
+}
+
+int stencil_plan_fold_coeffs(stencil_plan plan, int m, double* dense, int64_t cap) {
+    if (!plan || !dense) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (m < 1) return set_error(STENCIL_EINVAL, "fold_m must be >= 1");
+    if (m > STENCIL_MAX_FOLD) return set_error(STENCIL_EUNSUPPORTED, "fold_m > STENCIL_MAX_FOLD");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    const std::vector<double>& lam = folded(p, m);
+    if (cap < (int64_t)lam.size()) return set_error(STENCIL_EINVAL, "capacity too small");
+    std::copy(lam.begin(), lam.end(), dense);
+    return STENCIL_OK;
+}
+
+int stencil_workspace_size(stencil_plan plan, int64_t* bytes) {
+    if (!plan || !bytes) return set_error(STENCIL_EINVAL, "NULL argument");
+    *bytes = make_layout(reinterpret_cast<Plan*>(plan), 0, 1, 0).bytes;
+    return STENCIL_OK;
+}
+
+int stencil_plan_layout_dist(stencil_plan plan, int rank, int nranks, int halo,
+                             stencil_layout* out) {
+    if (!plan || !out) return set_error(STENCIL_EINVAL, "NULL argument");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (p->ndim < 2) return set_error(STENCIL_EUNSUPPORTED, "dist layouts need ndim >= 2");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(STENCIL_EINVAL, "bad rank/nranks");
+    if (halo < p->r) return set_error(STENCIL_EINVAL, "halo must be >= radius");
+    if (p->dims[0] % nranks) return set_error(STENCIL_EINVAL, "axis-0 extent not divisible by nranks");
+    if (nranks > 1 && p->dims[0] / nranks < halo)
+        return set_error(STENCIL_EINVAL, "slab thinner than the halo");
+    to_public(make_layout(p, rank, nranks, halo), out);
+    return STENCIL_OK;
+}
+
+int stencil_plan_last_launches(stencil_plan plan, int64_t* launches) {
+    if (!plan || !launches) return set_error(STENCIL_EINVAL, "NULL argument");
+    *launches = reinterpret_cast<Plan*>(plan)->last_launches;
+    return STENCIL_OK;
+}
+
+}  // extern "C"

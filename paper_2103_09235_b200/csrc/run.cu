@@ -1,0 +1,597 @@
+// run.cu — orchestration of a run: frozen-ring init,
+// floor(T/m) folded sweeps + T mod m single steps in Jacobi ping-pong
+// (P:410), the main-region sweep plus the exact boundary band per sweep, and
+// the slab-decomposed multi-GPU run with a per-sweep halo exchange
+// (NCCL send/recv on a comm stream, overlapped with the interior).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "internal.hpp"
+#include "sweep_params.cuh"
+
+namespace sb {
+
+static int ensure_device(Plan* p) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return cuda_error(e, "cudaGetDevice");
+    if (p->device != dev || p->sm_count <= 0) {
+        int sms = 0;
+        e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        if (e != cudaSuccess) return cuda_error(e, "cudaDeviceGetAttribute");
+        p->sm_count = sms;
+        p->device = dev;
+    }
+    return STENCIL_OK;
+}
+
+// Partition the local interior into the region where lambda^(m) is valid (at
+// distance >= (m-1) r from every FIXED face) and the band shell around it.
+static void split_band(const Layout3& L, int m, Box* main, std::vector<Box>* band) {
+    Box in;
+    for (int a = 0; a < 3; ++a) { in.lo[a] = 0; in.hi[a] = L.n[a]; }
+    const int64_t b = (int64_t)(m - 1) * L.r;
+    band->clear();
+    for (int a = 0; a < 3; ++a) {
+        int64_t bl = L.phys_lo[a] ? b : 0, bh = L.phys_hi[a] ? b : 0;
+        if (bl > 0) {
+            Box s = in;
+            s.hi[a] = std::min(in.hi[a], in.lo[a] + bl);
+            if (!s.empty()) band->push_back(s);
+            in.lo[a] = s.hi[a];
+        }
+        if (bh > 0) {
+            Box s = in;
+            s.lo[a] = std::max(in.lo[a], in.hi[a] - bh);
+            if (!s.empty()) band->push_back(s);
+            in.hi[a] = s.lo[a];
+        }
+    }
+    *main = in;
+}
+
+static Box clip0(Box b, int64_t z0, int64_t z1) {
+    b.lo[0] = std::max(b.lo[0], z0);
+    b.hi[0] = std::min(b.hi[0], z1);
+    return b;
+}
+
+struct SweepSpec {
+    int m;          // steps in this sweep
+    Variant v;      // evaluation of the main region
+};
+
+// Enqueue one sweep restricted to axis-0 range [z0, z1). Returns launches or <0.
+static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, const SweepSpec& s,
+                         int64_t z0, int64_t z1, void* stream) {
+    Box mainb;
+    std::vector<Box> band;
+    split_band(L, s.m, &mainb, &band);
+    int launches = 0;
+    SweepCall sc;
+    sc.src = src;
+    sc.dst = dst;
+    sc.L = &L;
+    Box mb = clip0(mainb, z0, z1);
+    if (!mb.empty()) sc.boxes.push_back(mb);
+    sc.q = s.v.q;
+    sc.stages = s.v.stages;
+    sc.coef = &folded(p, s.v.q);
+    sc.stream = stream;
+    int rc = launch_sweep(p, sc);
+    if (rc < 0) return rc;
+    launches += rc;
+    if (s.m > 1) {
+        BandCall bc;
+        bc.src = src;
+        bc.dst = dst;
+        bc.L = &L;
+        for (const Box& b : band) {
+            Box c = clip0(b, z0, z1);
+            if (!c.empty()) bc.boxes.push_back(c);
+        }
+        bc.m = s.m;
+        bc.stream = stream;
+        rc = launch_band(p, bc);
+        if (rc < 0) return rc;
+        launches += rc;
+    }
+    return launches;
+}
+
+static int resolve_variant(Plan* p, int m, int stages, Variant* v) {
+    if (m == 1) { *v = {1, 1}; return STENCIL_OK; }
+    if (stages == 0) {
+        *v = choose_variant(p, m);
+        if (!sweep_supported(p, v->q, v->stages)) {
+            // fall back to any compiled split of m
+            for (int s = 1; s <= m; ++s)
+                if (m % s == 0 && sweep_supported(p, m / s, s)) { *v = {m / s, s}; return STENCIL_OK; }
+            return set_error(STENCIL_EUNSUPPORTED, "no compiled evaluation for fold_m=" + std::to_string(m));
+        }
+        return STENCIL_OK;
+    }
+    if (stages < 1 || m % stages) return set_error(STENCIL_EINVAL, "stages must divide fold_m");
+    *v = {m / stages, stages};
+    if (!sweep_supported(p, v->q, v->stages))
+        return set_error(STENCIL_EUNSUPPORTED, "no compiled sweep for fold_m=" + std::to_string(m) +
+                                                   " stages=" + std::to_string(stages));
+    return STENCIL_OK;
+}
+
+static bool misaligned(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 127) != 0; }
+
+static int check_run_args(Plan* p, const void* in, void* out, int64_t T, int m, void* ws) {
+    if (!p) return set_error(STENCIL_EINVAL, "plan is NULL");
+    if (T < 0) return set_error(STENCIL_EINVAL, "T must be >= 0");
+    if (m < 1) return set_error(STENCIL_EINVAL, "fold_m must be >= 1");
+    if (m > STENCIL_MAX_FOLD) return set_error(STENCIL_EUNSUPPORTED, "fold_m > STENCIL_MAX_FOLD");
+    if (!in || !out) return set_error(STENCIL_EINVAL, "in/out is NULL");
+    if (in == out || (ws && (ws == in || ws == out))) return set_error(STENCIL_EINVAL, "in, out and workspace must not alias");
+    if (misaligned(in) || misaligned(out) || (ws && misaligned(ws)))
+        return set_error(STENCIL_EINVAL, "buffers must be 128-byte aligned");
+    if (p->boundary != STENCIL_BC_FIXED) return set_error(STENCIL_EUNSUPPORTED, "PERIODIC is not implemented on the GPU");
+    return STENCIL_OK;
+}
+
+// ------------------------------------------------------------------ 1D
+static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t T, int m, int stages, void* ws,
+                  void* stream) {
+    const int64_t cap = std::max<int64_t>(m, 128 / m * m);
+    int64_t nl = (T + cap - 1) / cap;
+    if (nl >= 2 && !ws) return set_error(STENCIL_EINVAL, "workspace required");
+    bool force_step = (stages == m && m > 1);
+    int rc = launch_ring_copy(p, in, out, &L, stream);
+    if (rc < 0) return rc;
+    int launches = rc;
+    if (nl >= 2) {
+        rc = launch_ring_copy(p, in, ws, &L, stream);
+        if (rc < 0) return rc;
+        launches += rc;
+    }
+    void* bufs[2] = {out, ws};
+    int64_t left = T;
+    for (int64_t j = 1; j <= nl; ++j) {
+        int64_t tb = std::min(cap, left);
+        left -= tb;
+        const void* src = j == 1 ? in : bufs[(nl - j + 1) % 2];
+        void* dst = bufs[(nl - j) % 2];
+        rc = launch_1d(p, src, dst, &L, tb, m, force_step ? 1 : 0, stream);
+        if (rc < 0) return rc;
+        launches += rc;
+    }
+    p->last_launches = launches;
+    return STENCIL_OK;
+}
+
+int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages, void* ws, void* stream) {
+    int rc = check_run_args(p, in, out, T, m, ws);
+    if (rc) return rc;
+    rc = ensure_device(p);
+    if (rc) return rc;
+    Layout3 L = make_layout(p, 0, 1, 0);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (T == 0) {
+        cudaError_t e = cudaMemcpyAsync(out, in, L.bytes, cudaMemcpyDeviceToDevice, st);
+        p->last_launches = 0;
+        return e == cudaSuccess ? STENCIL_OK : cuda_error(e, "cudaMemcpyAsync");
+    }
+    if (p->ndim == 1) return run_1d(p, L, in, out, T, m, stages, ws, stream);
+    Variant v;
+    rc = resolve_variant(p, m, stages, &v);
+    if (rc) return rc;
+    const int64_t nf = T / m, nr = T % m, n = nf + nr;
+    if (n >= 2 && !ws) return set_error(STENCIL_EINVAL, "workspace required when more than one sweep runs");
+    int launches = 0;
+    rc = launch_ring_copy(p, in, out, &L, stream);
+    if (rc < 0) return rc;
+    launches += rc;
+    if (n >= 2) {
+        rc = launch_ring_copy(p, in, ws, &L, stream);
+        if (rc < 0) return rc;
+        launches += rc;
+    }
+    void* bufs[2] = {out, ws};
+    for (int64_t j = 1; j <= n; ++j) {
+        SweepSpec s;
+        s.m = j <= nf ? m : 1;
+        s.v = j <= nf ? v : Variant{1, 1};
+        const void* src = j == 1 ? in : bufs[(n - j + 1) % 2];
+        void* dst = bufs[(n - j) % 2];
+        rc = enqueue_sweep(p, L, src, dst, s, 0, L.n[0], stream);
+        if (rc < 0) return rc;
+        launches += rc;
+    }
+    p->last_launches = launches;
+    return STENCIL_OK;
+}
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct NcclApi {
+    ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    bool ok = false;
+    std::string why;
+};
+
+static NcclApi& nccl() {
+    static NcclApi api;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) { api.why = std::string("cannot dlopen libnccl.so.2: ") + dlerror(); return; }
+#define LOAD(name, field)                                                           \
+    api.field = reinterpret_cast<decltype(api.field)>(dlsym(h, name));              \
+    if (!api.field) { api.why = std::string("missing NCCL symbol ") + name; return; }
+        LOAD("ncclGetUniqueId", GetUniqueId);
+        LOAD("ncclCommInitRank", CommInitRank);
+        LOAD("ncclCommDestroy", CommDestroy);
+        LOAD("ncclSend", Send);
+        LOAD("ncclRecv", Recv);
+        LOAD("ncclGroupStart", GroupStart);
+        LOAD("ncclGroupEnd", GroupEnd);
+        LOAD("ncclGetErrorString", GetErrorString);
+#undef LOAD
+        api.ok = true;
+    });
+    return api;
+}
+
+static int nccl_error(ncclResult_t r, const char* what) {
+    NcclApi& a = nccl();
+    return set_error(STENCIL_ENCCL, std::string(what) + ": " + (a.GetErrorString ? a.GetErrorString(r) : "?"));
+}
+
+}  // namespace sb
+
+struct stencil_comm_s {
+    ncclComm_t comm = nullptr;
+    int rank = 0, nranks = 1;
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t evA = nullptr, evC = nullptr;
+};
+
+namespace sb {
+
+// Exchange planes between neighbours: rank g sends its planes [0,hx) to g-1
+// and [n0-hx, n0) to g+1; it receives into [-hx, 0) and [n0, n0+hx).
+struct Exchange {
+    virtual ~Exchange() {}
+    virtual int begin(int j, void* stream) = 0;   // after phase A of sweep j is enqueued
+    virtual int end(void* stream) = 0;            // before sweep j+1
+};
+
+static int dist_layout_check(Plan* p, int rank, int nranks, int halo, int m, Layout3* L) {
+    if (p->ndim < 2) return set_error(STENCIL_EUNSUPPORTED, "dist runs need ndim >= 2");
+    if (p->dims[0] % nranks) return set_error(STENCIL_EINVAL, "axis-0 extent not divisible by nranks");
+    if (halo < m * p->r) return set_error(STENCIL_EINVAL, "halo must be >= fold_m * radius");
+    if (nranks > 1 && p->dims[0] / nranks < halo) return set_error(STENCIL_EINVAL, "slab thinner than the halo");
+    *L = make_layout(p, rank, nranks, halo);
+    return STENCIL_OK;
+}
+
+// One rank's share of a sweep, split in phase A (the planes neighbours need)
+// and phase B (the rest).
+static int sweep_phase(Plan* p, const Layout3& L, const void* src, void* dst, const SweepSpec& s, int rank,
+                       int nranks, int64_t hx, int phase, void* stream) {
+    const int64_t n0 = L.n[0];
+    bool has_lo = rank > 0, has_hi = rank < nranks - 1;
+    if (nranks == 1 || 2 * hx >= n0) {
+        if (phase == 0) return enqueue_sweep(p, L, src, dst, s, 0, n0, stream);
+        return 0;
+    }
+    int launches = 0, rc;
+    if (phase == 0) {
+        if (has_lo) {
+            rc = enqueue_sweep(p, L, src, dst, s, 0, hx, stream);
+            if (rc < 0) return rc;
+            launches += rc;
+        }
+        if (has_hi) {
+            rc = enqueue_sweep(p, L, src, dst, s, n0 - hx, n0, stream);
+            if (rc < 0) return rc;
+            launches += rc;
+        }
+        return launches;
+    }
+    int64_t z0 = has_lo ? hx : 0, z1 = has_hi ? n0 - hx : n0;
+    return enqueue_sweep(p, L, src, dst, s, z0, z1, stream);
+}
+
+static size_t plane_bytes(const Layout3& L) { return (size_t)L.stride[0] * L.esize; }
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+int stencil_fill_random(stencil_plan plan, void* buf, uint64_t seed, void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !buf) return set_error(STENCIL_EINVAL, "NULL argument");
+    int rc = ensure_device(p);
+    if (rc) return rc;
+    Layout3 L = make_layout(p, 0, 1, 0);
+    rc = launch_fill(p, buf, &L, seed, stream);
+    return rc < 0 ? rc : STENCIL_OK;
+}
+
+int stencil_fill_random_dist(stencil_plan plan, int rank, int nranks, int halo, void* buf, uint64_t seed,
+                             void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !buf) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(STENCIL_EINVAL, "bad rank/nranks");
+    Layout3 L;
+    int rc = dist_layout_check(p, rank, nranks, halo, 1, &L);
+    if (rc) return rc;
+    rc = ensure_device(p);
+    if (rc) return rc;
+    rc = launch_fill(p, buf, &L, seed, stream);
+    return rc < 0 ? rc : STENCIL_OK;
+}
+
+int stencil_run(stencil_plan plan, const void* in, void* out, int64_t T, int fold_m, void* workspace,
+                void* stream) {
+    return run_single(reinterpret_cast<Plan*>(plan), in, out, T, fold_m, 0, workspace, stream);
+}
+
+int stencil_run_ex(stencil_plan plan, const void* in, void* out, int64_t T, int fold_m, int stages,
+                   void* workspace, void* stream) {
+    return run_single(reinterpret_cast<Plan*>(plan), in, out, T, fold_m, stages, workspace, stream);
+}
+
+int stencil_run_host(stencil_plan plan, const void* in_host, void* out_host, int64_t T, int fold_m, int stages,
+                     void* dev_in, void* dev_out, void* workspace, void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !in_host || !out_host || !dev_in || !dev_out) return set_error(STENCIL_EINVAL, "NULL argument");
+    Layout3 L = make_layout(p, 0, 1, 0);
+    cudaStream_t st = (cudaStream_t)stream;
+    cudaError_t e = cudaMemcpyAsync(dev_in, in_host, L.bytes, cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync H2D");
+    int rc = run_single(p, dev_in, dev_out, T, fold_m, stages, workspace, stream);
+    if (rc) return rc;
+    e = cudaMemcpyAsync(out_host, dev_out, L.bytes, cudaMemcpyDeviceToHost, st);
+    if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync D2H");
+    return STENCIL_OK;
+}
+
+int stencil_comm_unique_id(unsigned char id[128]) {
+    if (!id) return set_error(STENCIL_EINVAL, "NULL argument");
+    NcclApi& a = nccl();
+    if (!a.ok) return set_error(STENCIL_ENCCL, a.why);
+    ncclUniqueId u;
+    ncclResult_t r = a.GetUniqueId(&u);
+    if (r != ncclSuccess) return nccl_error(r, "ncclGetUniqueId");
+    static_assert(sizeof(u) == 128, "ncclUniqueId size");
+    std::memcpy(id, &u, 128);
+    return STENCIL_OK;
+}
+
+int stencil_comm_create(stencil_comm* comm, const unsigned char id[128], int rank, int nranks) {
+    if (!comm || !id) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(STENCIL_EINVAL, "bad rank/nranks");
+    *comm = nullptr;
+    NcclApi& a = nccl();
+    if (!a.ok) return set_error(STENCIL_ENCCL, a.why);
+    stencil_comm_s* c = new stencil_comm_s();
+    c->rank = rank;
+    c->nranks = nranks;
+    ncclUniqueId u;
+    std::memcpy(&u, id, 128);
+    ncclResult_t r = a.CommInitRank(&c->comm, nranks, u, rank);
+    if (r != ncclSuccess) {
+        delete c;
+        return nccl_error(r, "ncclCommInitRank");
+    }
+    cudaError_t e = cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->evA, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&c->evC, cudaEventDisableTiming);
+    if (e != cudaSuccess) {
+        a.CommDestroy(c->comm);
+        delete c;
+        return cuda_error(e, "comm stream/events");
+    }
+    *comm = c;
+    return STENCIL_OK;
+}
+
+int stencil_comm_destroy(stencil_comm comm) {
+    if (!comm) return STENCIL_OK;
+    NcclApi& a = nccl();
+    if (comm->comm && a.ok) a.CommDestroy(comm->comm);
+    if (comm->evA) cudaEventDestroy(comm->evA);
+    if (comm->evC) cudaEventDestroy(comm->evC);
+    if (comm->cstream) cudaStreamDestroy(comm->cstream);
+    delete comm;
+    return STENCIL_OK;
+}
+
+static int nccl_exchange(Plan* p, stencil_comm_s* c, const Layout3& L, void* buf, int64_t hx, cudaStream_t st) {
+    NcclApi& a = nccl();
+    const ncclDataType_t dt = p->dtype == STENCIL_F64 ? ncclDouble : ncclFloat;
+    const size_t cnt = (size_t)hx * L.stride[0];
+    char* base = static_cast<char*>(buf);
+    const size_t pb = plane_bytes(L);
+    auto plane = [&](int64_t z) { return base + (size_t)(L.origin[0] + z) * pb; };
+    ncclResult_t r = a.GroupStart();
+    if (r != ncclSuccess) return nccl_error(r, "ncclGroupStart");
+    if (c->rank > 0) {
+        a.Send(plane(0), cnt, dt, c->rank - 1, c->comm, st);
+        a.Recv(plane(-hx), cnt, dt, c->rank - 1, c->comm, st);
+    }
+    if (c->rank < c->nranks - 1) {
+        a.Send(plane(L.n[0] - hx), cnt, dt, c->rank + 1, c->comm, st);
+        a.Recv(plane(L.n[0]), cnt, dt, c->rank + 1, c->comm, st);
+    }
+    r = a.GroupEnd();
+    if (r != ncclSuccess) return nccl_error(r, "ncclGroupEnd");
+    return STENCIL_OK;
+}
+
+int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void* buf, int halo, void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !comm || !buf) return set_error(STENCIL_EINVAL, "NULL argument");
+    Layout3 L;
+    int rc = dist_layout_check(p, comm->rank, comm->nranks, halo, 1, &L);
+    if (rc) return rc;
+    if (comm->nranks == 1) return STENCIL_OK;
+    return nccl_exchange(p, comm, L, buf, halo, (cudaStream_t)stream);
+}
+
+int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local, void* out_local, int64_t T,
+                     int fold_m, int stages, int halo, void* workspace, void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!comm) return set_error(STENCIL_EINVAL, "comm is NULL");
+    int rc = check_run_args(p, in_local, out_local, T, fold_m, workspace);
+    if (rc) return rc;
+    Layout3 L;
+    rc = dist_layout_check(p, comm->rank, comm->nranks, halo, fold_m, &L);
+    if (rc) return rc;
+    rc = ensure_device(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (T == 0) {
+        cudaError_t e = cudaMemcpyAsync(out_local, in_local, L.bytes, cudaMemcpyDeviceToDevice, st);
+        return e == cudaSuccess ? STENCIL_OK : cuda_error(e, "cudaMemcpyAsync");
+    }
+    Variant v;
+    rc = resolve_variant(p, fold_m, stages, &v);
+    if (rc) return rc;
+    const int64_t nf = T / fold_m, nr = T % fold_m, n = nf + nr;
+    if (n >= 2 && !workspace) return set_error(STENCIL_EINVAL, "workspace required");
+    const int64_t hx = (int64_t)fold_m * p->r;
+    int launches = 0;
+    rc = launch_ring_copy(p, in_local, out_local, &L, stream);
+    if (rc < 0) return rc;
+    launches += rc;
+    if (n >= 2) {
+        rc = launch_ring_copy(p, in_local, workspace, &L, stream);
+        if (rc < 0) return rc;
+        launches += rc;
+    }
+    void* bufs[2] = {out_local, workspace};
+    for (int64_t j = 1; j <= n; ++j) {
+        SweepSpec s;
+        s.m = j <= nf ? fold_m : 1;
+        s.v = j <= nf ? v : Variant{1, 1};
+        const void* src = j == 1 ? in_local : bufs[(n - j + 1) % 2];
+        void* dst = bufs[(n - j) % 2];
+        rc = sweep_phase(p, L, src, dst, s, comm->rank, comm->nranks, hx, 0, stream);
+        if (rc < 0) return rc;
+        launches += rc;
+        const bool xchg = comm->nranks > 1 && j < n;
+        if (xchg) {
+            cudaEventRecord(comm->evA, st);
+            cudaStreamWaitEvent(comm->cstream, comm->evA, 0);
+            rc = nccl_exchange(p, comm, L, dst, hx, comm->cstream);
+            if (rc) return rc;
+            cudaEventRecord(comm->evC, comm->cstream);
+        }
+        rc = sweep_phase(p, L, src, dst, s, comm->rank, comm->nranks, hx, 1, stream);
+        if (rc < 0) return rc;
+        launches += rc;
+        if (xchg) cudaStreamWaitEvent(st, comm->evC, 0);
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "run_dist");
+    p->last_launches = launches;
+    return STENCIL_OK;
+}
+
+int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void* const* in_locals, void* const* out_locals,
+                              int64_t T, int fold_m, int stages, int halo, void* const* workspaces, void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !in_locals || !out_locals || nranks < 1) return set_error(STENCIL_EINVAL, "bad argument");
+    std::vector<Layout3> Ls(nranks);
+    for (int g = 0; g < nranks; ++g) {
+        int rc = check_run_args(p, in_locals[g], out_locals[g], T, fold_m, workspaces ? workspaces[g] : nullptr);
+        if (rc) return rc;
+        rc = dist_layout_check(p, g, nranks, halo, fold_m, &Ls[g]);
+        if (rc) return rc;
+    }
+    int rc = ensure_device(p);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (T == 0) {
+        for (int g = 0; g < nranks; ++g) {
+            cudaError_t e = cudaMemcpyAsync(out_locals[g], in_locals[g], Ls[g].bytes, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync");
+        }
+        return STENCIL_OK;
+    }
+    Variant v;
+    rc = resolve_variant(p, fold_m, stages, &v);
+    if (rc) return rc;
+    const int64_t nf = T / fold_m, nr = T % fold_m, n = nf + nr;
+    if (n >= 2 && !workspaces) return set_error(STENCIL_EINVAL, "workspaces required");
+    const int64_t hx = (int64_t)fold_m * p->r;
+    int launches = 0;
+    for (int g = 0; g < nranks; ++g) {
+        rc = launch_ring_copy(p, in_locals[g], out_locals[g], &Ls[g], stream);
+        if (rc < 0) return rc;
+        if (n >= 2) {
+            if (!workspaces[g]) return set_error(STENCIL_EINVAL, "workspace required");
+            rc = launch_ring_copy(p, in_locals[g], workspaces[g], &Ls[g], stream);
+            if (rc < 0) return rc;
+        }
+    }
+    for (int64_t j = 1; j <= n; ++j) {
+        SweepSpec s;
+        s.m = j <= nf ? fold_m : 1;
+        s.v = j <= nf ? v : Variant{1, 1};
+        std::vector<const void*> srcs(nranks);
+        std::vector<void*> dsts(nranks);
+        for (int g = 0; g < nranks; ++g) {
+            void* bufs[2] = {out_locals[g], workspaces ? workspaces[g] : nullptr};
+            srcs[g] = j == 1 ? in_locals[g] : bufs[(n - j + 1) % 2];
+            dsts[g] = bufs[(n - j) % 2];
+            rc = sweep_phase(p, Ls[g], srcs[g], dsts[g], s, g, nranks, hx, 0, stream);
+            if (rc < 0) return rc;
+            launches += rc;
+        }
+        if (nranks > 1 && j < n) {
+            // the transport: device-to-device copies between the ranks' buffers
+            for (int g = 0; g < nranks; ++g) {
+                const Layout3& L = Ls[g];
+                const size_t pb = plane_bytes(L);
+                char* me = static_cast<char*>(dsts[g]);
+                if (g > 0) {
+                    const Layout3& Ln = Ls[g - 1];
+                    char* nb = static_cast<char*>(dsts[g - 1]);
+                    cudaMemcpyAsync(nb + (size_t)(Ln.origin[0] + Ln.n[0]) * pb, me + (size_t)L.origin[0] * pb,
+                                    (size_t)hx * pb, cudaMemcpyDeviceToDevice, st);
+                }
+                if (g < nranks - 1) {
+                    const Layout3& Ln = Ls[g + 1];
+                    char* nb = static_cast<char*>(dsts[g + 1]);
+                    cudaMemcpyAsync(nb + (size_t)(Ln.origin[0] - hx) * pb,
+                                    me + (size_t)(L.origin[0] + L.n[0] - hx) * pb, (size_t)hx * pb,
+                                    cudaMemcpyDeviceToDevice, st);
+                }
+            }
+        }
+        for (int g = 0; g < nranks; ++g) {
+            rc = sweep_phase(p, Ls[g], srcs[g], dsts[g], s, g, nranks, hx, 1, stream);
+            if (rc < 0) return rc;
+            launches += rc;
+        }
+    }
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "run_dist_emulated");
+    p->last_launches = launches;
+    return STENCIL_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,560 @@
+// sweep.cu — K-G1/K-G2: the streaming sweep of the main (folded-valid) region.
+//
+// One template evaluates one m-step sweep as `S` on-chip passes of the folded
+// weights lambda^(Q) (m = Q*S):
+//   S = 1      the folded sweep (Eq.2; vertical folding Eq.4 P:381-387 and
+//              horizontal folding Eq.5-6 P:390-406 collapse into one weighted
+//              sum over supp lambda^(m));
+//   Q = 1      the on-chip m-step temporal block ("time loop fusion", P:592,
+//              P:708; "multiple time steps computation in registers over the
+//              tiles ... without reloading");
+//   otherwise  S on-chip passes of a Q-step fold.
+//
+// B200 mapping:
+//  * The grid streams along its slowest axis (z in 3D, y in 2D).  Input planes
+//    (in-plane tile + halo) are staged into a ring of shared-memory slots by
+//    TMA (cp.async.bulk.tensor, one elected producer thread) with mbarrier
+//    full/empty double-buffering; out-of-allocation cells are zero-filled by
+//    TMA and are never used by a valid output.
+//  * Vertical folding (Eq.4) becomes a register sliding window along the
+//    stream axis: every loaded plane is multiplied by each lambda "slice" and
+//    added to the 2*Q*r+1 pending output planes held in registers, so each
+//    value is read from shared memory once per sweep, not once per tap.
+//  * Horizontal folding (Eq.5-6) becomes the in-plane combination: each thread
+//    reads its neighbourhood with 16-byte vector loads (double2/float4) and
+//    owns VX x VY outputs (register reuse between adjacent outputs = the
+//    paper's shifts reusing).
+//  * Stages > 1 hand each completed intermediate plane to the next stage
+//    through a double-buffered shared-memory plane (one named barrier per
+//    stage per plane); tiles overlap by the intermediate halo.
+//  * Cells of the frozen physical ring keep u0 at every intermediate level
+//    (R1); only tiles whose extent reaches the ring test for it.
+//  * Outputs are written with 16-byte vector stores.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+
+#include "internal.hpp"
+#include "ptx.cuh"
+#include "sweep_params.cuh"
+
+namespace sb {
+
+// ------------------------------------------------------------------ config
+template <typename T_, int ND_, int SHAPE_, int RR_, int Q_, int S_, int NTX_, int NTY_, int VY_, int PB_,
+          int NSLOT_>
+struct Cfg {
+    using T = T_;
+    static constexpr int ND = ND_, SHAPE = SHAPE_, RR = RR_, Q = Q_, S = S_;
+    static constexpr int NTX = NTX_, NTY = NTY_, VY = VY_, PB = PB_, NSLOT = NSLOT_;
+    static constexpr int VX = 16 / (int)sizeof(T);
+    static constexpr int RQ = Q * RR;
+    static constexpr int RQY = ND == 3 ? RQ : 0;
+    static constexpr int H = S * RQ;
+    static constexpr int NW = 2 * RQ + 1;
+    static constexpr int PX = (RQ + VX - 1) / VX * VX;
+    static constexpr int NV = (VX + 2 * PX) / VX;
+    static constexpr int NR = VY + 2 * RQY;
+    static constexpr int WX = NTX * VX, WY = NTY * VY;
+    static constexpr int HXO = ((S - 1) * RQ + VX - 1) / VX * VX;
+    static constexpr int HYO = (S - 1) * RQY;
+    static constexpr int WOX = WX - 2 * HXO, WOY = WY - 2 * HYO;
+    static constexpr int COLS = WX + 2 * PX;
+    static constexpr int NBX = (COLS + 255) / 256;
+    static constexpr int BX = ((COLS + NBX - 1) / NBX + VX - 1) / VX * VX;
+    static constexpr int ROWS = WY + 2 * RQY;
+    static constexpr int CHUNK = (PB * ROWS * BX + (128 / (int)sizeof(T)) - 1) / (128 / (int)sizeof(T)) *
+                                 (128 / (int)sizeof(T));
+    static constexpr int SLOT_ELEMS = NBX * CHUNK;
+    static constexpr uint32_t SLOT_BYTES = (uint32_t)(NBX * PB * ROWS * BX * sizeof(T));
+    static constexpr int LEV_ELEMS = ROWS * COLS;
+    static constexpr int NCONS = NTX * NTY;
+    static constexpr int NCW = NCONS / 32;
+    static constexpr int NTHREADS = NCONS + 32;
+    static constexpr int NC = ND == 3 ? NW * NW * NW : NW * NW;
+    static constexpr size_t SMEM = (size_t)NSLOT * SLOT_ELEMS * sizeof(T) +
+                                   (size_t)(S - 1) * 2 * LEV_ELEMS * sizeof(T) + 2 * NSLOT * 8;
+    static_assert(NCONS % 32 == 0, "consumer threads must be whole warps");
+    static_assert(WOX > 0 && WOY > 0, "tile too small for the halo");
+    static_assert(BX <= 256 && ROWS <= 256 && PB <= 256, "TMA box limit");
+    static_assert(ND == 3 || (NTY == 1 && VY == 1), "2D tiles are one row");
+};
+
+template <int SHAPE, int RR, int Q>
+__host__ __device__ constexpr bool in_support(int oz, int oy, int ox) {
+    // STAR: the Q-fold Minkowski sum of axis segments [-RR, RR]; BOX: the full box.
+    return SHAPE == STENCIL_BOX
+               ? true
+               : ((oz < 0 ? -oz : oz) + RR - 1) / RR + ((oy < 0 ? -oy : oy) + RR - 1) / RR +
+                         ((ox < 0 ? -ox : ox) + RR - 1) / RR <=
+                     Q;
+}
+
+__host__ __device__ constexpr int pmod(int a, int n) { return ((a % n) + n) % n; }
+
+template <typename T>
+struct VecT;
+template <>
+struct VecT<double> {
+    using V = double2;
+    static __device__ __forceinline__ void ld(const double* p, double* out) {
+        double2 v = *reinterpret_cast<const double2*>(p);
+        out[0] = v.x;
+        out[1] = v.y;
+    }
+    static __device__ __forceinline__ void st(double* p, const double* in) {
+        *reinterpret_cast<double2*>(p) = make_double2(in[0], in[1]);
+    }
+};
+template <>
+struct VecT<float> {
+    static __device__ __forceinline__ void ld(const float* p, float* out) {
+        float4 v = *reinterpret_cast<const float4*>(p);
+        out[0] = v.x;
+        out[1] = v.y;
+        out[2] = v.z;
+        out[3] = v.w;
+    }
+    static __device__ __forceinline__ void st(float* p, const float* in) {
+        *reinterpret_cast<float4*>(p) = make_float4(in[0], in[1], in[2], in[3]);
+    }
+};
+
+__device__ __forceinline__ double fmaT(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float fmaT(float a, float b, float c) { return __fmaf_rn(a, b, c); }
+
+template <class C>
+struct Consumer {
+    using T = typename C::T;
+    T acc[C::S][C::NW][C::VY][C::VX];
+    T nb[C::NR][C::NV * C::VX];
+
+    // FMA the neighbourhood `nb` of one level-J plane into stage J's window.
+    template <int J, int PH>
+    __device__ __forceinline__ void fold_plane(const T* __restrict__ coef) {
+        constexpr int RQ = C::RQ, RQY = C::RQY, NW = C::NW;
+#pragma unroll
+        for (int k = 0; k < NW; ++k) {
+            const int oz = RQ - k;
+            const int idx = pmod(PH - J * RQ - RQ + k, NW);
+#pragma unroll
+            for (int oy = -RQY; oy <= RQY; ++oy)
+#pragma unroll
+                for (int ox = -RQ; ox <= RQ; ++ox) {
+                    if (!in_support<C::SHAPE, C::RR, C::Q>(oz, oy, ox)) continue;
+                    const int ci = C::ND == 3 ? ((oz + RQ) * (2 * RQY + 1) + (oy + RQY)) * (2 * RQ + 1) + (ox + RQ)
+                                              : (oz + RQ) * (2 * RQ + 1) + (ox + RQ);
+                    const T c = coef[ci];
+#pragma unroll
+                    for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                        for (int vx = 0; vx < C::VX; ++vx)
+                            acc[J][idx][vy][vx] = fmaT(c, nb[vy + oy + RQY][vx + ox + C::PX], acc[J][idx][vy][vx]);
+                }
+        }
+    }
+};
+
+template <class C>
+__global__ void __launch_bounds__(C::NTHREADS)
+    sweep_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ SweepParams<typename C::T, C::NC> p) {
+    using T = typename C::T;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    T* slots = reinterpret_cast<T*>(smem_raw);
+    T* lev = slots + C::NSLOT * C::SLOT_ELEMS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(lev + (C::S - 1) * 2 * C::LEV_ELEMS);
+    uint64_t* empty = full + C::NSLOT;
+
+    // ---- tile decode
+    const int bid = blockIdx.x;
+    int bi = 0;
+#pragma unroll 1
+    while (bi + 1 < p.b.nbox && bid >= p.b.tiles_begin[bi + 1]) ++bi;
+    int t = bid - p.b.tiles_begin[bi];
+    const int ntx = p.b.tx[bi], nty = p.b.ty[bi];
+    const int itx = t % ntx;
+    t /= ntx;
+    const int ity = t % nty;
+    const int itz = t / nty;
+    const int blo0 = p.b.lo[bi][0], bhi0 = p.b.hi[bi][0];
+    const int blo1 = p.b.lo[bi][1], bhi1 = p.b.hi[bi][1];
+    const int blo2 = p.b.lo[bi][2], bhi2 = p.b.hi[bi][2];
+    const int ox0 = (blo2 - blo2 % C::VX) + itx * C::WOX;
+    const int cx0 = ox0 - C::HXO;
+    const int oy0 = blo1 + ity * C::WOY;
+    const int cy0 = oy0 - C::HYO;
+    const int z0 = blo0 + itz * p.b.zchunk[bi];
+    const int z1 = min(z0 + p.b.zchunk[bi], bhi0);
+    const int NPL = z1 - z0 + 2 * C::H;
+    const int NPLP = (NPL + C::NW - 1) / C::NW * C::NW;
+    const int nslot_total = (NPLP + C::PB - 1) / C::PB;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int s = 0; s < C::NSLOT; ++s) {
+            ptx::mbar_init(&full[s], 1);
+            ptx::mbar_init(&empty[s], C::NCW);
+        }
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+
+    // ---- producer warp: one elected thread streams planes with TMA
+    if (warp == C::NCW) {
+        if (lane == 0) {
+            ptx::prefetch_tmap(&tmap);
+            const int xs = (int)p.g.origin[2] + cx0 - C::PX;
+            const int ys = (int)p.g.origin[1] + cy0 - C::RQY;
+            const int zs = (int)p.g.origin[0] + z0 - C::H;
+#pragma unroll 1
+            for (int sq = 0; sq < nslot_total; ++sq) {
+                const int slot = sq % C::NSLOT, round = sq / C::NSLOT;
+                if (round > 0) ptx::mbar_wait(&empty[slot], (round - 1) & 1);
+                ptx::mbar_expect_tx(&full[slot], C::SLOT_BYTES);
+                T* dst = slots + slot * C::SLOT_ELEMS;
+#pragma unroll
+                for (int c = 0; c < C::NBX; ++c) {
+                    if (C::ND == 2)
+                        ptx::tma_load_2d(dst + c * C::CHUNK, &tmap, &full[slot], xs + c * C::BX, zs + sq * C::PB);
+                    else
+                        ptx::tma_load_3d(dst + c * C::CHUNK, &tmap, &full[slot], xs + c * C::BX, ys,
+                                         zs + sq * C::PB);
+                }
+            }
+        }
+        return;
+    }
+
+    // ---- consumers
+    const int tx = threadIdx.x % C::NTX, ty = threadIdx.x / C::NTX;
+    int off0[C::NV];
+#pragma unroll
+    for (int v = 0; v < C::NV; ++v) {
+        const int c = tx * C::VX + v * C::VX;
+        off0[v] = (c / C::BX) * C::CHUNK + (c % C::BX);
+    }
+    Consumer<C> cs;
+#pragma unroll
+    for (int s = 0; s < C::S; ++s)
+#pragma unroll
+        for (int k = 0; k < C::NW; ++k)
+#pragma unroll
+            for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                for (int vx = 0; vx < C::VX; ++vx) cs.acc[s][k][vy][vx] = T(0);
+
+    // Does this tile's computed extent reach a physical ring (frozen cells)?
+    bool edge = false;
+    if (C::S > 1) {
+        edge |= p.g.phys_lo[0] && (z0 - C::H < 0);
+        edge |= p.g.phys_hi[0] && (z1 + C::H > p.g.n[0]);
+        edge |= p.g.phys_lo[2] && (cx0 - C::PX < 0);
+        edge |= p.g.phys_hi[2] && (cx0 + C::WX + C::PX > p.g.n[2]);
+        if (C::ND == 3) {
+            edge |= p.g.phys_lo[1] && (cy0 - C::RQY < 0);
+            edge |= p.g.phys_hi[1] && (cy0 + C::WY + C::RQY > p.g.n[1]);
+        }
+    }
+    const T* __restrict__ src = p.src;
+    T* __restrict__ dst = p.dst;
+    const long long s0 = p.g.stride0, s1 = p.g.stride1;
+    const int gx = cx0 + tx * C::VX;          // first x of this thread's block
+    const int gy = cy0 + ty * C::VY;          // first y (3D)
+    const int xlo = max(ox0, blo2), xhi = min(ox0 + C::WOX, bhi2);
+    const int ylo = C::ND == 3 ? max(oy0, blo1) : 0, yhi = C::ND == 3 ? min(oy0 + C::WOY, bhi1) : 1;
+
+#pragma unroll 1
+    for (int g = 0; g < NPLP; g += C::NW) {
+        auto step = [&](auto PHc) {
+            constexpr int PH = decltype(PHc)::value;
+            const int i = g + PH;
+            // ---------------- stage 0: level-0 plane i from the TMA ring
+            {
+                const int sq = i / C::PB, pl = i % C::PB, slot = sq % C::NSLOT;
+                if (pl == 0) ptx::mbar_wait(&full[slot], (sq / C::NSLOT) & 1);
+                const T* base = slots + slot * C::SLOT_ELEMS + (pl * C::ROWS + ty * C::VY) * C::BX;
+#pragma unroll
+                for (int rr = 0; rr < C::NR; ++rr)
+#pragma unroll
+                    for (int v = 0; v < C::NV; ++v) VecT<T>::ld(base + rr * C::BX + off0[v], &cs.nb[rr][v * C::VX]);
+                if (pl == C::PB - 1) {
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(&empty[slot]);
+                }
+                cs.template fold_plane<0, PH>(p.coef);
+            }
+            // ---------------- stages 1..S-1 through shared-memory planes
+            auto stage = [&](auto Jc) {
+                constexpr int J = decltype(Jc)::value;
+                constexpr int done = pmod(PH - J * C::RQ, C::NW);
+                T v[C::VY][C::VX];
+#pragma unroll
+                for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                    for (int vx = 0; vx < C::VX; ++vx) {
+                        v[vy][vx] = cs.acc[J - 1][done][vy][vx];
+                        cs.acc[J - 1][done][vy][vx] = T(0);
+                    }
+                const int z = z0 - C::H + (i - J * C::RQ);
+                if (edge) {
+#pragma unroll
+                    for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                        for (int vx = 0; vx < C::VX; ++vx) {
+                            const int c3[3] = {z, gy + vy, gx + vx};
+                            bool outside = false, inframe = true;
+#pragma unroll
+                            for (int a = 0; a < 3; ++a) {
+                                if (C::ND == 2 && a == 1) continue;
+                                if (c3[a] < 0) {
+                                    if (p.g.phys_lo[a]) outside = true;
+                                    if (c3[a] < -p.g.lo_valid[a]) inframe = false;
+                                } else if (c3[a] >= p.g.n[a]) {
+                                    if (p.g.phys_hi[a]) outside = true;
+                                    if (c3[a] >= p.g.n[a] + p.g.hi_valid[a]) inframe = false;
+                                }
+                            }
+                            if (outside && inframe)
+                                v[vy][vx] = src[(p.g.origin[0] + z) * s0 + (p.g.origin[1] + gy + vy) * s1 +
+                                                p.g.origin[2] + gx + vx];
+                        }
+                }
+                T* lp = lev + ((J - 1) * 2 + (i & 1)) * C::LEV_ELEMS;
+#pragma unroll
+                for (int vy = 0; vy < C::VY; ++vy)
+                    VecT<T>::st(lp + (ty * C::VY + vy + C::RQY) * C::COLS + tx * C::VX + C::PX, v[vy]);
+                ptx::named_bar_sync(1, C::NCONS);
+                const T* base = lp + (ty * C::VY) * C::COLS + tx * C::VX;
+#pragma unroll
+                for (int rr = 0; rr < C::NR; ++rr)
+#pragma unroll
+                    for (int vv = 0; vv < C::NV; ++vv)
+                        VecT<T>::ld(base + rr * C::COLS + vv * C::VX, &cs.nb[rr][vv * C::VX]);
+                cs.template fold_plane<J, PH>(p.coef);
+            };
+            if constexpr (C::S > 1) stage(std::integral_constant<int, 1>{});
+            if constexpr (C::S > 2) stage(std::integral_constant<int, 2>{});
+            if constexpr (C::S > 3) stage(std::integral_constant<int, 3>{});
+            static_assert(C::S <= 4, "at most 4 on-chip stages");
+            // ---------------- output: level-S plane i - H
+            {
+                constexpr int done = pmod(PH - C::H, C::NW);
+                const int z = z0 - C::H + (i - C::H);
+                if (z >= z0 && z < z1) {
+#pragma unroll
+                    for (int vy = 0; vy < C::VY; ++vy) {
+                        const int y = gy + vy;
+                        if (y < ylo || y >= yhi) continue;
+                        T* op = dst + (p.g.origin[0] + z) * s0 + (p.g.origin[1] + y) * s1 + p.g.origin[2] + gx;
+                        if (gx >= xlo && gx + C::VX <= xhi) {
+                            VecT<T>::st(op, cs.acc[C::S - 1][done][vy]);
+                        } else {
+#pragma unroll
+                            for (int vx = 0; vx < C::VX; ++vx)
+                                if (gx + vx >= xlo && gx + vx < xhi) op[vx] = cs.acc[C::S - 1][done][vy][vx];
+                        }
+                    }
+                }
+#pragma unroll
+                for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                    for (int vx = 0; vx < C::VX; ++vx) cs.acc[C::S - 1][done][vy][vx] = T(0);
+            }
+        };
+        [&]<int... PHs>(std::integer_sequence<int, PHs...>) {
+            (step(std::integral_constant<int, PHs>{}), ...);
+        }(std::make_integer_sequence<int, C::NW>{});
+    }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+template <class C>
+static int make_tmap(const Layout3& L, const void* base, CUtensorMap* map) {
+    auto enc = encode_fn();
+    if (!enc) return set_error(STENCIL_ECUDA, "cuTensorMapEncodeTiled not available from the driver");
+    using T = typename C::T;
+    CUtensorMapDataType dt = sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    cuuint64_t gdim[3];
+    cuuint64_t gstr[2];
+    cuuint32_t box[3];
+    cuuint32_t estr[3] = {1, 1, 1};
+    int rank;
+    if (C::ND == 2) {
+        rank = 2;
+        gdim[0] = L.ext[2];
+        gdim[1] = L.ext[0];
+        gstr[0] = L.stride[0] * sizeof(T);
+        box[0] = C::BX;
+        box[1] = C::PB;
+    } else {
+        rank = 3;
+        gdim[0] = L.ext[2];
+        gdim[1] = L.ext[1];
+        gdim[2] = L.ext[0];
+        gstr[0] = L.stride[1] * sizeof(T);
+        gstr[1] = L.stride[0] * sizeof(T);
+        box[0] = C::BX;
+        box[1] = C::ROWS;
+        box[2] = C::PB;
+    }
+    CUresult r = enc(map, dt, rank, const_cast<void*>(base), gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(STENCIL_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    return STENCIL_OK;
+}
+
+template <class C>
+static int occupancy() {
+    static int occ = -1;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        if (C::SMEM > 48 * 1024)
+            cudaFuncSetAttribute(sweep_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
+        int o = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, sweep_kernel<C>, C::NTHREADS, C::SMEM) !=
+            cudaSuccess)
+            o = 1;
+        occ = std::max(1, o);
+    });
+    return occ;
+}
+
+template <class C>
+static int launch_cfg(Plan* p, const SweepCall& c) {
+    using T = typename C::T;
+    const Layout3& L = *c.L;
+    SweepParams<T, C::NC> prm;
+    std::memset(&prm, 0, sizeof(prm));
+    prm.src = static_cast<const T*>(c.src);
+    prm.dst = static_cast<T*>(c.dst);
+    fill_geom(L, &prm.g);
+    if ((int)c.coef->size() != C::NC) return set_error(STENCIL_EUNSUPPORTED, "coefficient table size mismatch");
+    for (int i = 0; i < C::NC; ++i) prm.coef[i] = static_cast<T>((*c.coef)[i]);
+
+    std::vector<Box> boxes;
+    for (const Box& b : c.boxes)
+        if (!b.empty()) boxes.push_back(b);
+    if (boxes.empty()) return 0;
+    if ((int)boxes.size() > MAXBOX) return set_error(STENCIL_EUNSUPPORTED, "too many boxes");
+    const int occ = occupancy<C>();
+    const int target = std::max(1, p->sm_count * occ);
+    int64_t xy_total = 0;
+    std::vector<int> ntx(boxes.size()), nty(boxes.size());
+    int64_t vol_total = 0;
+    for (size_t i = 0; i < boxes.size(); ++i) {
+        const Box& b = boxes[i];
+        int64_t x0 = b.lo[2] - b.lo[2] % C::VX;
+        ntx[i] = (int)((b.hi[2] - x0 + C::WOX - 1) / C::WOX);
+        nty[i] = C::ND == 3 ? (int)((b.hi[1] - b.lo[1] + C::WOY - 1) / C::WOY) : 1;
+        xy_total += (int64_t)ntx[i] * nty[i];
+        vol_total += b.volume();
+    }
+    prm.b.nbox = (int)boxes.size();
+    int64_t tiles = 0;
+    for (size_t i = 0; i < boxes.size(); ++i) {
+        const Box& b = boxes[i];
+        int64_t zlen = b.hi[0] - b.lo[0];
+        int64_t xy = (int64_t)ntx[i] * nty[i];
+        // chunks so that the whole launch is about one wave of resident CTAs
+        double share = vol_total > 0 ? double(b.volume()) / double(vol_total) : 1.0;
+        int64_t want = std::max<int64_t>(1, (int64_t)(target * share) / std::max<int64_t>(1, xy));
+        int64_t minlen = std::max<int64_t>(8, 4 * C::H);
+        int64_t nch = std::min<int64_t>(want, std::max<int64_t>(1, zlen / minlen));
+        int64_t zc = (zlen + nch - 1) / nch;
+        nch = (zlen + zc - 1) / zc;
+        for (int a = 0; a < 3; ++a) {
+            prm.b.lo[i][a] = (int)b.lo[a];
+            prm.b.hi[i][a] = (int)b.hi[a];
+        }
+        prm.b.tx[i] = ntx[i];
+        prm.b.ty[i] = nty[i];
+        prm.b.zchunk[i] = (int)zc;
+        prm.b.tiles_begin[i] = (int)tiles;
+        tiles += xy * nch;
+    }
+    prm.b.tiles_begin[boxes.size()] = (int)tiles;
+    (void)xy_total;
+    CUtensorMap map;
+    int rc = make_tmap<C>(L, c.src, &map);
+    if (rc) return rc;
+    sweep_kernel<C><<<(unsigned)tiles, C::NTHREADS, C::SMEM, (cudaStream_t)c.stream>>>(map, prm);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "sweep_kernel launch");
+    return 1;
+}
+
+// ------------------------------------------------------------------ dispatch
+// Tile configurations:
+//  2D: one row of NTX threads x VX (= 16 B) columns; PB rows per TMA slot.
+//  3D: NTX x NTY threads, each 2 x VY outputs, one plane per TMA slot.
+template <typename T, int SHAPE, int Q, int S>
+using Cfg2 = Cfg<T, 2, SHAPE, 1, Q, S, 128, 1, 1, 4, 4>;
+template <typename T, int SHAPE, int Q, int S>
+using Cfg3 = Cfg<T, 3, SHAPE, 1, Q, S, 32, 8, 2, 1, 4>;
+
+using LaunchFn = int (*)(Plan*, const SweepCall&);
+
+template <typename T, int SHAPE>
+static LaunchFn pick2(int q, int s) {
+    if (q == 1 && s == 1) return launch_cfg<Cfg2<T, SHAPE, 1, 1>>;
+    if (q == 2 && s == 1) return launch_cfg<Cfg2<T, SHAPE, 2, 1>>;
+    if (q == 4 && s == 1) return launch_cfg<Cfg2<T, SHAPE, 4, 1>>;
+    if (q == 1 && s == 2) return launch_cfg<Cfg2<T, SHAPE, 1, 2>>;
+    if (q == 1 && s == 4) return launch_cfg<Cfg2<T, SHAPE, 1, 4>>;
+    if (q == 2 && s == 2) return launch_cfg<Cfg2<T, SHAPE, 2, 2>>;
+    return nullptr;
+}
+template <typename T, int SHAPE>
+static LaunchFn pick3(int q, int s) {
+    if (q == 1 && s == 1) return launch_cfg<Cfg3<T, SHAPE, 1, 1>>;
+    if (q == 2 && s == 1) return launch_cfg<Cfg3<T, SHAPE, 2, 1>>;
+    if (q == 1 && s == 2) return launch_cfg<Cfg3<T, SHAPE, 1, 2>>;
+    return nullptr;
+}
+
+static LaunchFn pick(int dtype, int nd, int shape, int r, int q, int s) {
+    if (r != 1) return nullptr;
+    if (nd == 2) {
+        if (dtype == STENCIL_F64) return shape == STENCIL_STAR ? pick2<double, STENCIL_STAR>(q, s) : pick2<double, STENCIL_BOX>(q, s);
+        return shape == STENCIL_STAR ? pick2<float, STENCIL_STAR>(q, s) : pick2<float, STENCIL_BOX>(q, s);
+    }
+    if (nd == 3) {
+        if (dtype == STENCIL_F64) return shape == STENCIL_STAR ? pick3<double, STENCIL_STAR>(q, s) : pick3<double, STENCIL_BOX>(q, s);
+        return shape == STENCIL_STAR ? pick3<float, STENCIL_STAR>(q, s) : pick3<float, STENCIL_BOX>(q, s);
+    }
+    return nullptr;
+}
+
+bool sweep_supported(const Plan* p, int q, int s) { return pick(p->dtype, p->ndim, p->shape, p->r, q, s) != nullptr; }
+
+int launch_sweep(Plan* p, const SweepCall& c) {
+    LaunchFn fn = pick(p->dtype, p->ndim, p->shape, p->r, c.q, c.stages);
+    if (!fn)
+        return set_error(STENCIL_EUNSUPPORTED, "no compiled sweep for ndim=" + std::to_string(p->ndim) +
+                                                   " r=" + std::to_string(p->r) + " q=" + std::to_string(c.q) +
+                                                   " stages=" + std::to_string(c.stages));
+    return fn(p, c);
+}
+
+}  // namespace sb

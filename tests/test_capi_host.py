@@ -1,0 +1,114 @@
+"""CPU-side tests of the C-ABI library: it loads, exports every symbol the
+header declares, validates arguments, and its host-side coefficient-folding
+generator agrees with the (independently written, pinned) oracle fold.
+No compute call here needs a GPU."""
+import os
+import re
+import subprocess
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from paper_2103_09235_b200 import _lib
+from paper_2103_09235_b200 import Plan, StencilError
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(ROOT, "include", "stencil_b200.h")
+
+
+def header_symbols():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(stencil_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    out = subprocess.run(["nm", "-D", "--defined-only", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(line.split()[-1] for line in out.splitlines() if line.strip())
+    for s in syms:
+        assert s in exported, s
+        assert hasattr(lib, s)
+    # the binding mirrors the header one to one
+    assert sorted(_lib.SIGNATURES) == syms
+
+
+def test_version_and_error_channel():
+    lib = _lib.load()
+    assert b"sm_100a" in lib.stencil_version()
+    with pytest.raises(StencilError) as e:
+        Plan((8, 8), 1, "star", [1.0] * 4)      # 2D STAR needs 5 taps
+    assert e.value.code == -1 and "canonical tap count 5" in str(e.value)
+
+
+@pytest.mark.parametrize("bad", [dict(dims=(0, 8)), dict(radius=0), dict(dims=(4, 4, 4, 4))])
+def test_plan_create_rejects(bad):
+    kw = dict(dims=(8, 8), radius=1, shape="star", coeffs=[0.2] * 5)
+    kw.update(bad)
+    with pytest.raises((StencilError, KeyError, ValueError)):
+        Plan(**kw)
+
+
+def test_canonical_taps_match_oracle():
+    for nd in (1, 2, 3):
+        for shape in ("star", "box"):
+            k = len(oracle.taps(nd, 1, 0 if shape == "star" else 1))
+            p = Plan((5,) * nd, 1, shape, synth.weights(k, 1))
+            assert p.taps() == oracle.taps(nd, 1, 0 if shape == "star" else 1)
+
+
+@pytest.mark.parametrize("nd,shape,m", [(1, "star", 2), (1, "star", 5), (2, "star", 2), (2, "star", 4),
+                                        (2, "box", 2), (2, "box", 4), (3, "star", 2), (3, "box", 2),
+                                        (2, "star", 3), (1, "star", 8)])
+def test_fold_generator_matches_oracle_fold(nd, shape, m):
+    sh = 0 if shape == "star" else 1
+    offs = oracle.taps(nd, 1, sh)
+    w = synth.weights(len(offs), 9)
+    p = Plan((7,) * nd, 1, shape, w)
+    lib_lam = p.fold_coeffs(m)
+    ref = oracle.fold_ref(oracle.dense_from_taps(nd, 1, offs, w), m)
+    assert lib_lam.shape == ref.shape
+    assert np.max(np.abs(lib_lam - ref)) <= 1e-15 * np.abs(ref).sum()
+    assert np.count_nonzero(lib_lam) == np.count_nonzero(ref)
+
+
+def test_fold_generator_paper_example_exact():
+    """Integer weights: exact agreement with the paper's worked example."""
+    from conftest import read_golden
+    golden = np.array([[float(x) for x in row] for row in read_golden("fold_2d9p_uniform_m2.txt")])
+    p = Plan((5, 5), 1, "box", [1.0] * 9)
+    assert np.array_equal(p.fold_coeffs(2), golden)
+    with pytest.raises(StencilError):
+        p.fold_coeffs(0)
+
+
+def test_layout_alignment_and_views():
+    import torch
+    for dt, es in (("f64", 8), ("f32", 4)):
+        p = Plan((100, 37), 1, "star", synth.weights(5, 1), dtype=dt)
+        L = p.layout
+        assert L.elem_bytes == es
+        assert (L.origin[-1] * es) % 128 == 0          # interior x = 0 is 128-byte aligned
+        assert (L.stride[0] * es) % 128 == 0           # row pitch multiple of 128 bytes
+        assert L.extent[0] == 102 and L.origin[0] == 1
+        buf = p.empty("cpu")
+        fr = p.frame_view(buf)
+        assert tuple(fr.shape) == (102, 39)
+        u0 = synth.u0_frame((100, 37), 1, 2)
+        b2 = p.from_frame(u0, "cpu")
+        assert np.array_equal(p.frame_view(b2).numpy(), u0.astype(np.float64 if dt == "f64" else np.float32))
+        assert torch.count_nonzero(b2) == np.count_nonzero(u0)
+
+
+def test_dist_layout():
+    p = Plan((64, 32, 16), 1, "star", synth.weights(7, 1))
+    with pytest.raises(StencilError):
+        p.layout_dist(0, 3, 2)          # 64 not divisible by 3
+    L0 = p.layout_dist(0, 4, 2)
+    L3 = p.layout_dist(3, 4, 2)
+    assert L0.interior[0] == 16 and L0.origin[0] == 2 and L0.extent[0] == 20
+    assert L3.global_offset0 == 48

@@ -1,0 +1,195 @@
+"""GPU parity: the CUDA path (through the C-ABI) vs the fp64 CPU oracle on the
+same seeded inputs, element by element over the whole padded frame, at sizes
+that span several tiles and ragged tails.  Tolerances (BASELINE.json
+north_star): max|d| <= 1e-11 max|u0| (fp64), <= 2e-5 max|u0| (fp32)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"f64": 1e-11, "f32": 2e-5}
+
+
+def _plan(dims, shape, dtype, w):
+    from paper_2103_09235_b200 import Plan
+    return Plan(dims, 1, shape, w, dtype)
+
+
+def run_case(dims, shape, dtype, T, m, stages, seed_w=1, seed_u=2, u0=None, w=None):
+    nd = len(dims)
+    sh = oracle.STAR if shape == "star" else oracle.BOX
+    offs = oracle.taps(nd, 1, sh)
+    if w is None:
+        w = synth.weights(len(offs), seed_w)
+    if u0 is None:
+        u0 = synth.u0_frame(dims, 1, seed_u)
+    ref = oracle.run(dims, 1, offs, w, u0, T)
+    plan = _plan(dims, shape, dtype, w)
+    a = plan.from_frame(u0)
+    b = plan.empty()
+    ws = plan.empty()
+    plan.run(a, b, T, m, workspace=ws, stages=stages)
+    torch.cuda.synchronize()
+    got = plan.frame_view(b).cpu().double().numpy()
+    # `in` is never written
+    assert np.array_equal(plan.frame_view(a).cpu().double().numpy(),
+                          u0.astype(np.float64 if dtype == "f64" else np.float32).astype(np.float64))
+    return got, ref, u0, plan
+
+
+CASES_2D = [(m, s) for (m, s) in [(1, 1), (2, 1), (4, 1), (2, 2), (4, 2), (4, 4)]]
+
+
+@pytest.mark.parametrize("shape", ["star", "box"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("m,stages", CASES_2D)
+@pytest.mark.parametrize("T", [7, 8])
+def test_parity_2d(shape, dtype, m, stages, T):
+    dims = (70, 523)
+    got, ref, u0, _ = run_case(dims, shape, dtype, T, m, stages)
+    err = np.max(np.abs(got - ref))
+    assert err <= TOL[dtype] * np.max(np.abs(u0)), err
+
+
+@pytest.mark.parametrize("shape", ["star", "box"])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("m,stages", [(1, 1), (2, 1), (2, 2)])
+@pytest.mark.parametrize("T", [5, 6])
+def test_parity_3d(shape, dtype, m, stages, T):
+    dims = (19, 37, 75)
+    got, ref, u0, _ = run_case(dims, shape, dtype, T, m, stages)
+    err = np.max(np.abs(got - ref))
+    assert err <= TOL[dtype] * np.max(np.abs(u0)), err
+
+
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("n,T,m,stages", [(1000, 37, 1, 1), (1000, 37, 2, 1), (1000, 37, 2, 2),
+                                          (100000, 100, 1, 1), (100000, 100, 2, 1), (100000, 100, 4, 1),
+                                          (5000, 300, 2, 1), (50, 9, 4, 1)])
+def test_parity_1d(dtype, n, T, m, stages):
+    got, ref, u0, _ = run_case((n,), "star", dtype, T, m, stages)
+    err = np.max(np.abs(got - ref))
+    assert err <= TOL[dtype] * np.max(np.abs(u0)), err
+
+
+@pytest.mark.parametrize("dims,shape,m,stages,T", [
+    ((40, 300), "box", 1, 1, 6), ((40, 300), "box", 2, 1, 6), ((40, 300), "box", 4, 1, 7),
+    ((40, 300), "star", 4, 2, 7), ((40, 300), "star", 4, 4, 5), ((12, 20, 70), "box", 2, 1, 6),
+    ((12, 20, 70), "star", 2, 2, 7), ((333,), "star", 2, 1, 7)])
+def test_exact_dyadic_bitwise(dims, shape, m, stages, T):
+    """Dyadic weights and field: every partial sum is exact in fp64, so the GPU
+    (any accumulation order, folded or stepwise, band included) must equal
+    the oracle bit for bit."""
+    nd = len(dims)
+    k = len(oracle.taps(nd, 1, oracle.STAR if shape == "star" else oracle.BOX))
+    w = synth.dyadic_weights(k, seed=5)
+    u0 = synth.dyadic_field(tuple(n + 2 for n in dims), seed=6)
+    got, ref, _, _ = run_case(dims, shape, "f64", T, m, stages, u0=u0, w=w)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("dims,shape,m,T", [((3, 5), "box", 4, 9), ((2, 3, 4), "star", 2, 5),
+                                            ((1, 50), "star", 2, 6), ((50, 1), "box", 4, 8),
+                                            ((1, 1, 9), "box", 2, 4), ((7, 9), "star", 4, 1),
+                                            ((6, 200), "star", 2, 0), ((1,), "star", 2, 5)])
+def test_edge_cases(dims, shape, m, T):
+    got, ref, u0, _ = run_case(dims, shape, "f64", T, m, 0)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(u0))
+
+
+def test_device_generator_matches_host_generator():
+    for dims, shape in [((37, 301), "star"), ((9, 17, 70), "box"), ((777,), "star")]:
+        k = len(oracle.taps(len(dims), 1, oracle.STAR if shape == "star" else oracle.BOX))
+        for dt in ("f64", "f32"):
+            plan = _plan(dims, shape, dt, synth.weights(k, 1))
+            buf = plan.empty()
+            plan.fill_random(buf, 2)
+            torch.cuda.synchronize()
+            got = plan.frame_view(buf).cpu().numpy()
+            ref = synth.u0_frame(dims, 1, 2).astype(got.dtype)
+            assert np.array_equal(got, ref)
+
+
+def test_dist_generator_and_layout():
+    dims = (64, 20, 40)
+    plan = _plan(dims, "star", "f64", synth.weights(7, 1))
+    G, halo = 4, 2
+    for g in range(G):
+        L = plan.layout_dist(g, G, halo)
+        buf = plan.empty(layout=L)
+        plan.fill_random_dist(g, G, halo, buf, 2)
+        torch.cuda.synchronize()
+        # local planes [-1, n+1) on axis 0 map to global padded rows g*16 + ...
+        lo = L.global_offset0
+        full = synth.u0_frame(dims, 1, 2)
+        for zl in range(-1, L.interior[0] + 1):
+            zg = lo + zl
+            if zg < -1 or zg > dims[0]:
+                continue
+            plane = buf.as_strided((dims[1] + 2, dims[2] + 2), L.stride[1:],
+                                   (L.origin[0] + zl) * L.stride[0] + (L.origin[1] - 1) * L.stride[1] + L.origin[2] - 1)
+            assert np.array_equal(plane.cpu().numpy(), full[zg + 1])
+
+
+@pytest.mark.parametrize("dims,shape,dtype,m,stages,T,G", [
+    ((64, 300), "box", "f32", 2, 1, 9, 2), ((64, 300), "box", "f32", 4, 2, 9, 4),
+    ((48, 20, 70), "star", "f64", 2, 1, 7, 4), ((48, 20, 70), "box", "f64", 2, 2, 6, 2),
+    ((64, 300), "star", "f64", 1, 1, 5, 8)])
+def test_dist_emulated_bitwise_equals_single(dims, shape, dtype, m, stages, T, G):
+    """The slab-decomposed algorithm (all ranks on this GPU, exchange by D2D copies,
+    the same kernels and boxes as stencil_run_dist) is bitwise equal to 1 GPU
+    and within tolerance of the oracle."""
+    nd = len(dims)
+    k = len(oracle.taps(nd, 1, oracle.STAR if shape == "star" else oracle.BOX))
+    w = synth.weights(k, 1)
+    plan = _plan(dims, shape, dtype, w)
+    a = plan.empty()
+    plan.fill_random(a, 2)
+    b, ws = plan.empty(), plan.empty()
+    plan.run(a, b, T, m, workspace=ws, stages=stages)
+    halo = max(m, 2)
+    ins, outs, wss, Ls = [], [], [], []
+    for g in range(G):
+        L = plan.layout_dist(g, G, halo)
+        Ls.append(L)
+        t = plan.empty(layout=L)
+        plan.fill_random_dist(g, G, halo, t, 2)
+        ins.append(t)
+        outs.append(plan.empty(layout=L))
+        wss.append(plan.empty(layout=L))
+    plan.run_dist_emulated(ins, outs, T, m, halo, wss, stages=stages)
+    torch.cuda.synchronize()
+    single = plan.interior_view(b).cpu().numpy()
+    per = dims[0] // G
+    for g in range(G):
+        loc = plan.interior_view(outs[g], Ls[g]).cpu().numpy()
+        assert np.array_equal(loc, single[g * per:(g + 1) * per]), g
+    ref = oracle.run(dims, 1, oracle.taps(nd, 1, oracle.STAR if shape == "star" else oracle.BOX), w,
+                     synth.u0_frame(dims, 1, 2), T)
+    err = np.max(np.abs(plan.frame_view(b).cpu().double().numpy() - ref))
+    assert err <= TOL[dtype]
+
+
+def test_errors_and_launch_count():
+    from paper_2103_09235_b200 import StencilError
+    dims = (64, 64)
+    plan = _plan(dims, "star", "f64", synth.weights(5, 1))
+    a, b = plan.empty(), plan.empty()
+    with pytest.raises(StencilError):
+        plan.run(a, a, 4, 1, workspace=b)            # aliasing
+    with pytest.raises(StencilError):
+        plan.run(a, b, -1, 1, workspace=None)
+    with pytest.raises(StencilError):
+        plan.run(a, b, 4, 0, workspace=None)
+    with pytest.raises(StencilError):
+        plan.run(a, b, 8, 2, workspace=None)         # needs a workspace
+    with pytest.raises(StencilError):
+        plan.run(a, b, 8, 4, workspace=plan.empty(), stages=3)   # 3 does not divide 4
+    plan.fill_random(a, 2)
+    plan.run(a, b, 8, 2, workspace=plan.empty())
+    torch.cuda.synchronize()
+    assert plan.last_launches >= 4 + 1
