@@ -1,0 +1,415 @@
+#!/usr/bin/env python
+"""bench.py — GStencil/s of the B200 folded stencil sweep (arXiv 2103.09235).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c1..c5] [--fold-m M] [--stages S]
+
+A "step" is one pass of the whole hot path over one batch of synthetic input:
+stencil_run of T time steps (floor(T/m) folded sweeps + band + remainder) on
+the config's grid, inputs resident in HBM.  Default workload: BASELINE.json
+configs[1] = 2D5P star fp64 8192x8192, T = 200 (fits one GPU).  For N > 1
+GPUs (torchrun, one process per GPU) the grid is slab-decomposed along its
+slowest axis with N x the rows (weak scaling: 8192 rows per GPU) and a per
+sweep NCCL halo exchange (stencil_run_dist).
+
+The JSON line carries the device-timed value (max over ranks), the e2e number
+through the C-ABI with HOST buffers (stencil_run_host: H2D + run + D2H per
+step), the live roofline of the dominant kernel (the main-region sweep, timed
+with CUDA events on its launch stream inside the timed region), clocks seen by
+nvidia-smi during the timed region, and the CPU oracle's throughput on a
+bounded sample (rank 0, N = 1 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+METRIC = "GStencil/s (point-updates/s) fp64 and % of HBM roofline at 1/2/4/8 B200"
+UNIT = "GStencil/s"
+
+CONFIGS = {
+    "c1": dict(name="1D3P heat fp64 N=100000 T=100", dims=(100000,), shape="star", dtype="f64", T=100, ms=(1, 2)),
+    "c2": dict(name="2D5P star fp64 8192x8192 T=200", dims=(8192, 8192), shape="star", dtype="f64", T=200,
+               ms=(1, 2, 4)),
+    "c3": dict(name="2D9P box fp32 16384x16384 T=200", dims=(16384, 16384), shape="box", dtype="f32", T=200,
+               ms=(1, 2, 4)),
+    "c4": dict(name="3D7P star fp64 512^3 T=100", dims=(512, 512, 512), shape="star", dtype="f64", T=100,
+               ms=(1, 2)),
+    "c5": dict(name="3D27P box fp64 768x768x384 T=100", dims=(384, 768, 768), shape="box", dtype="f64", T=100,
+               ms=(1, 2)),
+}
+SAMPLE = {  # oracle sub-window of each workload for the CPU baseline / reference arm
+    "c1": (100000,), "c2": (1024, 1024), "c3": (1024, 1024), "c4": (96, 96, 96), "c5": (64, 64, 64),
+}
+
+
+def env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+    REASONS = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+
+    def __init__(self, index):
+        self.samples = []
+        self.t0 = self.t1 = None
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(index), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == len(self.FIELDS):
+                self.samples.append((time.time(), parts))
+
+    def start(self):
+        self.t0 = time.time()
+
+    def stop(self):
+        self.t1 = time.time()
+        time.sleep(0.25)
+        if self.proc:
+            self.proc.terminate()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        win = [p for t, p in self.samples if self.t0 and self.t1 and self.t0 - 0.1 <= t <= self.t1 + 0.1]
+        if not win:
+            win = [p for _, p in self.samples]
+
+        def num(x):
+            try:
+                return float(x)
+            except ValueError:
+                return None
+        sm = [num(p[0]) for p in win if num(p[0]) is not None]
+        mx = [num(p[1]) for p in win if num(p[1]) is not None]
+        reasons = sorted({self.REASONS[i] for p in win for i in range(4) if p[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(win)}
+
+
+def gpu_index(local_rank):
+    cvd = os.environ.get("CUDA_VISIBLE_DEVICES")
+    if cvd:
+        ids = [c.strip() for c in cvd.split(",") if c.strip()]
+        if local_rank < len(ids):
+            return ids[local_rank]
+    return str(local_rank)
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return d, "measured"
+    except (OSError, ValueError):
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0}, "fallback"
+
+
+def traffic_lookup(key):
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f).get(key)
+    except (OSError, ValueError):
+        return None
+
+
+# ----------------------------------------------------------------------------- CPU oracle
+def oracle_sample_run(cfg_key, target_s):
+    """Time the CPU oracle (as it stands) on a sub-window of the workload's field."""
+    import oracle
+    import synth
+    cfg = CONFIGS[cfg_key]
+    dims = cfg["dims"]
+    nd = len(dims)
+    sub = SAMPLE[cfg_key]
+    offs = oracle.taps(nd, 1, oracle.STAR if cfg["shape"] == "star" else oracle.BOX)
+    w = synth.weights(len(offs), synth.DEFAULT_SEED_W)
+    lo = [(n - s) // 2 for n, s in zip(dims, sub)]
+    u0 = synth.u0_block(dims, 1, lo, [l + s + 2 for l, s in zip(lo, sub)], synth.DEFAULT_SEED_U)
+    t = time.perf_counter()
+    oracle.run(sub, 1, offs, w, u0, 2)
+    t2 = max(1e-4, time.perf_counter() - t) / 2
+    T = int(max(1, min(cfg["T"], round(target_s / t2))))
+    return sub, offs, w, u0, T
+
+
+def oracle_time(sub, offs, w, u0, T):
+    import oracle
+    t = time.perf_counter()
+    oracle.run(sub, 1, offs, w, u0, T)
+    return time.perf_counter() - t
+
+
+def cpu_baseline(cfg_key, target_s=12.0):
+    import oracle
+    sub, offs, w, u0, T = oracle_sample_run(cfg_key, target_s)
+    dt = oracle_time(sub, offs, w, u0, T)
+    pts = 1
+    for n in sub:
+        pts *= n
+    return {"value": pts * T / dt / 1e9, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+            "sample": "%s sub-window of the %s field, T=%d steps (fp64 naive loops, %.1f s)" % (
+                "x".join(map(str, sub)), CONFIGS[cfg_key]["name"], T, dt)}
+
+
+def run_reference(args):
+    rank = env_int("RANK", 0)
+    if rank != 0:
+        return 0
+    import oracle
+    cfg = CONFIGS[args.config]
+    per_step = max(0.5, min(6.0, 150.0 / max(1, args.steps + args.warmup)))
+    sub, offs, w, u0, T = oracle_sample_run(args.config, per_step)
+    for _ in range(args.warmup):
+        oracle_time(sub, offs, w, u0, T)
+    tot = 0.0
+    for _ in range(args.steps):
+        tot += oracle_time(sub, offs, w, u0, T)
+    pts = 1
+    for n in sub:
+        pts *= n
+    value = pts * T * args.steps / tot / 1e9
+    sample = "%s sub-window of the %s field, T=%d steps per step" % ("x".join(map(str, sub)), cfg["name"], T)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": tot / args.steps * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": cfg["name"], "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": oracle.max_threads(), "kind": "oracle",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2103_09235_b200 import Plan
+    from paper_2103_09235_b200.dist import make_comm
+
+    rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = CONFIGS[args.config]
+    dims = list(cfg["dims"])
+    if world > 1:
+        dims[0] *= world            # weak scaling: the config's rows per GPU
+    nd = len(dims)
+    ms = [args.fold_m] if args.fold_m else list(cfg["ms"])
+    k = {(1, "star"): 3, (2, "star"): 5, (2, "box"): 9, (3, "star"): 7, (3, "box"): 27}[(nd, cfg["shape"])]
+    w = synth.weights(k, synth.DEFAULT_SEED_W)
+    plan = Plan(dims, 1, cfg["shape"], w, cfg["dtype"])
+    T = cfg["T"]
+    halo = max(ms)
+    comm = None
+    if world > 1:
+        L = plan.layout_dist(rank, world, halo)
+        a, b, ws = (plan.empty(layout=L) for _ in range(3))
+        plan.fill_random_dist(rank, world, halo, a, synth.DEFAULT_SEED_U)
+        comm = make_comm(dev)
+    else:
+        L = plan.layout
+        a, b, ws = plan.empty(), plan.empty(), plan.empty()
+        plan.fill_random(a, synth.DEFAULT_SEED_U)
+    stream = torch.cuda.current_stream()
+
+    def step(m, stages):
+        if world > 1:
+            plan.run_dist(comm, a, b, T, m, halo, ws, stages)
+        else:
+            plan.run(a, b, T, m, ws, stages)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(m, stages, n):
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(n):
+            step(m, stages)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        return allmax(e0.elapsed_time(e1) / n)
+
+    points = 1
+    for n in dims:
+        points *= n
+    # --- variants: every fold_m of the config (2 quick steps each); the best is the headline
+    variants = []
+    for m in ms:
+        step(m, args.stages)
+        t_ms = timed(m, args.stages, 2)
+        variants.append({"fold_m": m, "stages": args.stages, "ms_per_step": t_ms,
+                         "gstencil_s": points * T / (t_ms * 1e-3) / 1e9})
+    best = min(variants, key=lambda v: v["ms_per_step"])
+    m = best["fold_m"]
+    for _ in range(args.warmup):
+        step(m, args.stages)
+    torch.cuda.synchronize()
+    clocks = ClockSampler(gpu_index(local)) if rank == 0 else None
+    time.sleep(0.3)
+    # --- timed region (kernel events on, so the dominant kernel is timed live)
+    plan.timing_reset()
+    plan.set_timing(True)
+    barrier()
+    torch.cuda.synchronize()
+    if clocks:
+        clocks.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches = 0
+    e0.record(stream)
+    for _ in range(args.steps):
+        step(m, args.stages)
+        launches += plan.last_launches
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    if clocks:
+        clocks.stop()
+    plan.set_timing(False)
+    ms_step = allmax(e0.elapsed_time(e1) / args.steps)
+    kmain, kband = plan.timing(0), plan.timing(1)
+    plan.timing_reset()
+    value = points * T / (ms_step * 1e-3) / 1e9          # whole job (global points)
+
+    # --- e2e through the public API with host buffers
+    h2d = d2h = L.bytes
+    in_host = plan.empty("cpu", layout=L, pin_memory=True)
+    out_host = plan.empty("cpu", layout=L, pin_memory=True)
+    in_host.copy_(a.cpu())
+    ke = max(1, min(args.steps, 5))
+
+    def e2e_step():
+        if world > 1:
+            a.copy_(in_host, non_blocking=True)
+            plan.run_dist(comm, a, b, T, m, halo, ws, args.stages)
+            out_host.copy_(b, non_blocking=True)
+        else:
+            plan.run_host(in_host, out_host, T, m, a, b, ws, args.stages)
+    e2e_step()
+    torch.cuda.synchronize()
+    barrier()
+    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    x0.record(stream)
+    for _ in range(ke):
+        e2e_step()
+    x1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    e2e_ms = allmax(x0.elapsed_time(x1) / ke)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    peaks, peak_kind = measured_peaks()
+    esize = 8 if cfg["dtype"] == "f64" else 4
+    from paper_2103_09235_b200.api import Plan as _P  # noqa: F401
+    avg_ms = kmain["ms"] / max(1, kmain["launches"])
+    bytes_per_launch = kmain["bytes"] / max(1, kmain["launches"])
+    ach = bytes_per_launch / (avg_ms * 1e-3) / 1e9 if avg_ms > 0 else None
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    sm_max = float(peaks.get("sm_max_mhz", 1965.0))
+    fma_per_clk = 64 if esize == 8 else 128
+    fma_peak = 148 * fma_per_clk * sm_max * 1e6 / 1e12            # T FMA/s
+    fma_ach = kmain["fmas"] / max(1, kmain["launches"]) / (avg_ms * 1e-3) / 1e12 if avg_ms > 0 else None
+    frac_h = ach / hbm_peak if ach else None
+    frac_f = fma_ach / fma_peak if fma_ach else None
+    alu_bound = frac_f is not None and frac_h is not None and frac_f > frac_h
+    key = "%s/m%d/s%d" % (args.config, m, args.stages)
+    roof = {"bound": "alu" if alu_bound else "hbm",
+            "achieved": (fma_ach if alu_bound else ach), "peak": (fma_peak if alu_bound else hbm_peak),
+            "unit": "TFMA/s" if alu_bound else "GB/s",
+            "frac": (frac_f if alu_bound else frac_h),
+            "traffic": traffic_lookup(key),
+            "kernel": "sweep_kernel (main region, fold_m=%d)" % m,
+            "peak_kind": peak_kind if not alu_bound else "derived: 148 SM x %d FMA/clk x %.0f MHz" % (fma_per_clk, sm_max),
+            "hbm": {"achieved_gbs": ach, "peak_gbs": hbm_peak, "frac": frac_h},
+            "fma": {"achieved_tfma_s": fma_ach, "peak_tfma_s": fma_peak, "frac": frac_f},
+            "launches": kmain["launches"], "avg_launch_ms": avg_ms, "bytes_per_launch": bytes_per_launch,
+            "kernel_share_of_step": kmain["ms"] / (ms_step * args.steps) if ms_step > 0 else None,
+            "band": {"ms": kband["ms"], "launches": kband["launches"]}}
+    cl = clocks.summary() if clocks else {}
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
+            "config": {"workload": cfg["name"] + (" x%d rows (slab per GPU)" % world if world > 1 else ""),
+                       "dims": dims, "T": T, "fold_m": m, "stages": args.stages or "auto",
+                       "l2": "inputs larger than L2 (%.0f MB per buffer vs 126 MB)" % (L.bytes / 1e6),
+                       "parallelism": "slab%d" % world if world > 1 else "single"},
+            "gpu_launches": launches,
+            "e2e": {"value": points * T / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+            "roofline": roof,
+            "clocks": cl,
+            "variants": variants}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args.config)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c2")
+    ap.add_argument("--fold-m", type=int, default=0, help="0 = best of the config's fold_m set")
+    ap.add_argument("--stages", type=int, default=0, help="0 = the plan's choice")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -173,6 +173,21 @@ int stencil_run_host(stencil_plan plan, const void *in_host, void *out_host, int
 /* Number of kernel launches the last run on this plan enqueued (host count). */
 int stencil_plan_last_launches(stencil_plan plan, int64_t *launches);
 
+/*
+ * Measurement support.  While timing is enabled, every kernel launch of the
+ * main-region sweep (kind 0; the 1D on-chip kernel for ndim = 1) and of the
+ * boundary band (kind 1) is bracketed by CUDA events recorded on the launch
+ * stream.  stencil_plan_timing waits for those events and returns, for one
+ * kind, the summed kernel time (ms), the number of launches, the algorithmic
+ * bytes (2 * elem_bytes per output point: one read + one write per sweep) and
+ * the algorithmic FMAs (per output point: stages * |supp lambda^(q)|) of the
+ * launches recorded since the last reset.  Host only bookkeeping + event sync.
+ */
+int stencil_plan_set_timing(stencil_plan plan, int enable);
+int stencil_plan_timing(stencil_plan plan, int kind, double *ms, int64_t *launches, int64_t *bytes,
+                        int64_t *fmas);
+int stencil_plan_timing_reset(stencil_plan plan);
+
 /* ---------------------------------------------------------------- multi-GPU
  * Slab decomposition along axis 0 (the slowest axis), one process per GPU
  * (SURVEY §8(e)).  Rank g owns interior planes [g*N0/G, (g+1)*N0/G) plus

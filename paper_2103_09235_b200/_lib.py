@@ -38,6 +38,10 @@ SIGNATURES = {
     "stencil_run_ex": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp]),
     "stencil_run_host": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp, c_vp, c_vp]),
     "stencil_plan_last_launches": (c_int, [c_vp, ctypes.POINTER(c_i64)]),
+    "stencil_plan_set_timing": (c_int, [c_vp, c_int]),
+    "stencil_plan_timing": (c_int, [c_vp, c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64),
+                                    ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
+    "stencil_plan_timing_reset": (c_int, [c_vp]),
     "stencil_comm_unique_id": (c_int, [ctypes.c_char_p]),
     "stencil_comm_create": (c_int, [ctypes.POINTER(c_vp), ctypes.c_char_p, c_int, c_int]),
     "stencil_comm_destroy": (c_int, [c_vp]),

@@ -173,6 +173,21 @@ class Plan:
         check(self._lib.stencil_plan_last_launches(self._h, ctypes.byref(n)))
         return n.value
 
+    # ---------------------------------------------------------------- measurement
+    def set_timing(self, enable: bool):
+        check(self._lib.stencil_plan_set_timing(self._h, 1 if enable else 0))
+
+    def timing(self, kind: int = 0) -> dict:
+        """Event-timed kernel time of the recorded launches of `kind` (0 main
+        sweep / 1D kernel, 1 band): ms, launches, algorithmic bytes and FMAs."""
+        ms, n, by, fm = ctypes.c_double(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+        check(self._lib.stencil_plan_timing(self._h, int(kind), ctypes.byref(ms), ctypes.byref(n), ctypes.byref(by),
+                                            ctypes.byref(fm)))
+        return {"ms": ms.value, "launches": n.value, "bytes": by.value, "fmas": fm.value}
+
+    def timing_reset(self):
+        check(self._lib.stencil_plan_timing_reset(self._h))
+
     # ---------------------------------------------------------------- multi-GPU
     def fill_random_dist(self, rank, nranks, halo, buf, seed, stream=None):
         check(self._lib.stencil_fill_random_dist(self._h, rank, nranks, halo, _ptr(buf), int(seed), _stream(stream)))

@@ -56,8 +56,17 @@ struct Plan {
     std::map<int, std::vector<double>> lam;
     std::mutex mu;
     int64_t last_launches = 0;
+    // measurement support (stencil_plan_set_timing)
+    bool timing = false;
+    struct TimingRec { void* a; void* b; int kind; int64_t bytes; int64_t fmas; };
+    std::vector<TimingRec> recs;
+    std::vector<void*> event_pool;
     int sm_count = 0;
     int device = -1;
+    // dynamic-schedule scratch (device, plan-owned; 8 bytes per segment)
+    void* sched = nullptr;
+    int64_t sched_words = 0;
+    unsigned int epoch = 0;
 };
 
 const std::vector<double>& folded(Plan* p, int q);   // cached lambda^(q)
@@ -103,14 +112,15 @@ int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void
 // K-G0 seeded field over the frame (global padded index).
 int launch_fill(Plan* p, void* buf, const Layout3* L, uint64_t seed, void* stream);
 
+// Measurement: bracket a launch with events when timing is enabled.
+struct TimedScope {
+    Plan* p; void* stream; int kind; int64_t bytes, fmas; void* a = nullptr;
+    TimedScope(Plan* p_, void* s, int k, int64_t b, int64_t f);
+    ~TimedScope();
+};
+
 // ------------------------------------------------------------------ run
 int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages, void* ws,
                void* stream);
-
-struct Transport {
-    virtual ~Transport() {}
-    // Exchange: for every rank, send planes [lo,hi) of `bufs[rank]` to the
-    // neighbour's ghost planes. Implementation-specific.
-};
 
 }  // namespace sb

@@ -8,6 +8,8 @@
 #include <map>
 #include <new>
 
+#include <cuda_runtime.h>
+
 #include "internal.hpp"
 
 namespace sb {
@@ -270,7 +272,16 @@ int stencil_plan_create(stencil_plan* plan, int ndim, const int64_t* dims, int r
 }
 
 int stencil_plan_destroy(stencil_plan plan) {
-    delete reinterpret_cast<Plan*>(plan);
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (p) {
+        for (const auto& r : p->recs) {
+            cudaEventDestroy((cudaEvent_t)r.a);
+            cudaEventDestroy((cudaEvent_t)r.b);
+        }
+        for (void* e : p->event_pool) cudaEventDestroy((cudaEvent_t)e);
+        if (p->sched) cudaFree(p->sched);
+    }
+    delete p;
     return STENCIL_OK;
 }
 

@@ -16,6 +16,33 @@
 
 namespace sb {
 
+// ------------------------------------------------------------------ timing
+static void* take_event(Plan* p) {
+    if (!p->event_pool.empty()) {
+        void* e = p->event_pool.back();
+        p->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e = nullptr;
+    if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+    return e;
+}
+
+TimedScope::TimedScope(Plan* p_, void* s, int k, int64_t b, int64_t f)
+    : p(p_), stream(s), kind(k), bytes(b), fmas(f) {
+    if (!p->timing) return;
+    a = take_event(p);
+    if (a) cudaEventRecord((cudaEvent_t)a, (cudaStream_t)stream);
+}
+
+TimedScope::~TimedScope() {
+    if (!p->timing || !a) return;
+    void* b = take_event(p);
+    if (!b) return;
+    cudaEventRecord((cudaEvent_t)b, (cudaStream_t)stream);
+    p->recs.push_back({a, b, kind, bytes, fmas});
+}
+
 static int ensure_device(Plan* p) {
     int dev = 0;
     cudaError_t e = cudaGetDevice(&dev);
@@ -83,7 +110,13 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
     sc.stages = s.v.stages;
     sc.coef = &folded(p, s.v.q);
     sc.stream = stream;
-    int rc = launch_sweep(p, sc);
+    int rc;
+    {
+        const int64_t pts = mb.volume();
+        TimedScope ts(p, stream, 0, 2 * L.esize * pts,
+                      pts * s.v.stages * support_size(p->ndim, p->shape, p->r, s.v.q));
+        rc = launch_sweep(p, sc);
+    }
     if (rc < 0) return rc;
     launches += rc;
     if (s.m > 1) {
@@ -97,6 +130,9 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
         }
         bc.m = s.m;
         bc.stream = stream;
+        int64_t pts = 0;
+        for (const Box& b : bc.boxes) pts += b.volume();
+        TimedScope ts(p, stream, 1, 2 * L.esize * pts, pts * s.m * (int64_t)p->w.size());
         rc = launch_band(p, bc);
         if (rc < 0) return rc;
         launches += rc;
@@ -161,7 +197,12 @@ static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t 
         left -= tb;
         const void* src = j == 1 ? in : bufs[(nl - j + 1) % 2];
         void* dst = bufs[(nl - j) % 2];
-        rc = launch_1d(p, src, dst, &L, tb, m, force_step ? 1 : 0, stream);
+        {
+            TimedScope ts(p, stream, 0, 2 * L.esize * L.n[2],
+                          L.n[2] * (force_step ? tb * 3 : (tb / m) * support_size(1, p->shape, p->r, m) +
+                                                              (tb % m) * (int64_t)p->w.size()));
+            rc = launch_1d(p, src, dst, &L, tb, m, force_step ? 1 : 0, stream);
+        }
         if (rc < 0) return rc;
         launches += rc;
     }
@@ -340,6 +381,50 @@ int stencil_fill_random_dist(stencil_plan plan, int rank, int nranks, int halo, 
     if (rc) return rc;
     rc = launch_fill(p, buf, &L, seed, stream);
     return rc < 0 ? rc : STENCIL_OK;
+}
+
+int stencil_plan_set_timing(stencil_plan plan, int enable) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p) return set_error(STENCIL_EINVAL, "NULL argument");
+    p->timing = enable != 0;
+    return STENCIL_OK;
+}
+
+int stencil_plan_timing(stencil_plan plan, int kind, double* ms, int64_t* launches, int64_t* bytes,
+                        int64_t* fmas) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !ms || !launches || !bytes || !fmas) return set_error(STENCIL_EINVAL, "NULL argument");
+    double t = 0;
+    int64_t n = 0, by = 0, fm = 0;
+    for (const auto& rec : p->recs) {
+        if (rec.kind != kind) continue;
+        cudaError_t e = cudaEventSynchronize((cudaEvent_t)rec.b);
+        if (e != cudaSuccess) return cuda_error(e, "cudaEventSynchronize");
+        float x = 0;
+        e = cudaEventElapsedTime(&x, (cudaEvent_t)rec.a, (cudaEvent_t)rec.b);
+        if (e != cudaSuccess) return cuda_error(e, "cudaEventElapsedTime");
+        t += x;
+        ++n;
+        by += rec.bytes;
+        fm += rec.fmas;
+    }
+    *ms = t;
+    *launches = n;
+    *bytes = by;
+    *fmas = fm;
+    return STENCIL_OK;
+}
+
+int stencil_plan_timing_reset(stencil_plan plan) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p) return set_error(STENCIL_EINVAL, "NULL argument");
+    for (const auto& rec : p->recs) {
+        cudaEventSynchronize((cudaEvent_t)rec.b);
+        p->event_pool.push_back(rec.a);
+        p->event_pool.push_back(rec.b);
+    }
+    p->recs.clear();
+    return STENCIL_OK;
 }
 
 int stencil_run(stencil_plan plan, const void* in, void* out, int64_t T, int fold_m, void* workspace,

@@ -79,7 +79,7 @@ struct Cfg {
     static constexpr int NTHREADS = NCONS + 32;
     static constexpr int NC = ND == 3 ? NW * NW * NW : NW * NW;
     static constexpr size_t SMEM = (size_t)NSLOT * SLOT_ELEMS * sizeof(T) +
-                                   (size_t)(S - 1) * 2 * LEV_ELEMS * sizeof(T) + 2 * NSLOT * 8;
+                                   (size_t)(S - 1) * 2 * LEV_ELEMS * sizeof(T) + 2 * NSLOT * 8 + NSLOT * 32;
     static_assert(NCONS % 32 == 0, "consumer threads must be whole warps");
     static_assert(WOX > 0 && WOY > 0, "tile too small for the halo");
     static_assert(BX <= 256 && ROWS <= 256 && PB <= 256, "TMA box limit");
@@ -161,6 +161,48 @@ struct Consumer {
     }
 };
 
+// Per-slot metadata written by the producer before the slot's TMA is issued
+// (ordered by the mbarrier's release/acquire), read by the consumers.
+struct SlotMeta {
+    int z_first;   // interior plane index of the slot's first plane
+    int col;       // global column id
+    int out_lo;    // outputs of this run are stored for planes [out_lo, out_hi)
+    int out_hi;
+    int flags;     // 1 = restart (new run: reset accumulators), 2 = end
+};
+constexpr int META_RESTART = 1, META_END = 2;
+
+__device__ __forceinline__ unsigned long long seg_pack(unsigned e, int nx, int en) {
+    return ((unsigned long long)(e & 0xFFFFu) << 48) | ((unsigned long long)(nx & 0xFFFFFF) << 24) |
+           (unsigned long long)(en & 0xFFFFFF);
+}
+
+// Segment s -> box, column, initial [lo, hi) (planes relative to the box's lo[0]).
+__device__ __forceinline__ void seg_init(const DevBoxes& b, int s, int* box, int* col, int* lo, int* hi) {
+    int bi = 0;
+    while (bi + 1 < b.nbox && s >= b.seg_begin[bi + 1]) ++bi;
+    const int local = s - b.seg_begin[bi];
+    const int ncol = b.tx[bi] * b.ty[bi];
+    const int pz = local / ncol, c = local % ncol;
+    const int zlen = b.hi[bi][0] - b.lo[bi][0];
+    *box = bi;
+    *col = b.col_begin[bi] + c;
+    *lo = min(pz * b.zchunk[bi], zlen);
+    *hi = min(*lo + b.zchunk[bi], zlen);
+}
+
+__device__ __forceinline__ void seg_state(const DevSched& sc, const DevBoxes& b, int s, unsigned long long* w,
+                                          int* nx, int* en) {
+    *w = *reinterpret_cast<volatile unsigned long long*>(&sc.seg[s]);
+    if ((unsigned)(*w >> 48) != (sc.epoch & 0xFFFFu)) {
+        int bx, c;
+        seg_init(b, s, &bx, &c, nx, en);
+    } else {
+        *nx = (int)((*w >> 24) & 0xFFFFFF);
+        *en = (int)(*w & 0xFFFFFF);
+    }
+}
+
 template <class C>
 __global__ void __launch_bounds__(C::NTHREADS)
     sweep_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ SweepParams<typename C::T, C::NC> p) {
@@ -170,30 +212,7 @@ __global__ void __launch_bounds__(C::NTHREADS)
     T* lev = slots + C::NSLOT * C::SLOT_ELEMS;
     uint64_t* full = reinterpret_cast<uint64_t*>(lev + (C::S - 1) * 2 * C::LEV_ELEMS);
     uint64_t* empty = full + C::NSLOT;
-
-    // ---- tile decode
-    const int bid = blockIdx.x;
-    int bi = 0;
-#pragma unroll 1
-    while (bi + 1 < p.b.nbox && bid >= p.b.tiles_begin[bi + 1]) ++bi;
-    int t = bid - p.b.tiles_begin[bi];
-    const int ntx = p.b.tx[bi], nty = p.b.ty[bi];
-    const int itx = t % ntx;
-    t /= ntx;
-    const int ity = t % nty;
-    const int itz = t / nty;
-    const int blo0 = p.b.lo[bi][0], bhi0 = p.b.hi[bi][0];
-    const int blo1 = p.b.lo[bi][1], bhi1 = p.b.hi[bi][1];
-    const int blo2 = p.b.lo[bi][2], bhi2 = p.b.hi[bi][2];
-    const int ox0 = (blo2 - blo2 % C::VX) + itx * C::WOX;
-    const int cx0 = ox0 - C::HXO;
-    const int oy0 = blo1 + ity * C::WOY;
-    const int cy0 = oy0 - C::HYO;
-    const int z0 = blo0 + itz * p.b.zchunk[bi];
-    const int z1 = min(z0 + p.b.zchunk[bi], bhi0);
-    const int NPL = z1 - z0 + 2 * C::H;
-    const int NPLP = (NPL + C::NW - 1) / C::NW * C::NW;
-    const int nslot_total = (NPLP + C::PB - 1) / C::PB;
+    SlotMeta* meta = reinterpret_cast<SlotMeta*>(empty + C::NSLOT);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -206,33 +225,188 @@ __global__ void __launch_bounds__(C::NTHREADS)
     }
     __syncthreads();
 
-    // ---- producer warp: one elected thread streams planes with TMA
+    // Column id -> tile geometry (compute region origin cx0/cy0, output clip).
+    auto col_geom = [&](int col, int* bx, int* cx0, int* cy0, int* xlo, int* xhi, int* ylo, int* yhi) {
+        int bi = 0;
+        while (bi + 1 < p.b.nbox && col >= p.b.col_begin[bi + 1]) ++bi;
+        const int c = col - p.b.col_begin[bi];
+        const int itx = c % p.b.tx[bi], ity = c / p.b.tx[bi];
+        const int blo2 = p.b.lo[bi][2];
+        const int ox0 = (blo2 - blo2 % C::VX) + itx * C::WOX;
+        const int oy0 = p.b.lo[bi][1] + ity * C::WOY;
+        *bx = bi;
+        *cx0 = ox0 - C::HXO;
+        *cy0 = oy0 - C::HYO;
+        *xlo = max(ox0, blo2);
+        *xhi = min(ox0 + C::WOX, p.b.hi[bi][2]);
+        *ylo = C::ND == 3 ? max(oy0, p.b.lo[bi][1]) : 0;
+        *yhi = C::ND == 3 ? min(oy0 + C::WOY, p.b.hi[bi][1]) : 1;
+    };
+
+    // ================================================================ producer warp
     if (warp == C::NCW) {
-        if (lane == 0) {
-            ptx::prefetch_tmap(&tmap);
-            const int xs = (int)p.g.origin[2] + cx0 - C::PX;
-            const int ys = (int)p.g.origin[1] + cy0 - C::RQY;
-            const int zs = (int)p.g.origin[0] + z0 - C::H;
-#pragma unroll 1
-            for (int sq = 0; sq < nslot_total; ++sq) {
+        const DevSched& sc = p.sc;
+        const int myseg = blockIdx.x;
+        int sq = 0;
+        auto put = [&](const SlotMeta& m) {
+            if (lane == 0) {
                 const int slot = sq % C::NSLOT, round = sq / C::NSLOT;
                 if (round > 0) ptx::mbar_wait(&empty[slot], (round - 1) & 1);
-                ptx::mbar_expect_tx(&full[slot], C::SLOT_BYTES);
-                T* dst = slots + slot * C::SLOT_ELEMS;
+                meta[slot] = m;
+                if (m.flags & META_END) {
+                    ptx::mbar_arrive(&full[slot]);
+                } else {
+                    int bx, cx0, cy0, a, b2, c2, d2;
+                    col_geom(m.col, &bx, &cx0, &cy0, &a, &b2, &c2, &d2);
+                    const int xs = (int)p.g.origin[2] + cx0 - C::PX;
+                    const int ys = (int)p.g.origin[1] + cy0 - C::RQY;
+                    const int zs = (int)p.g.origin[0] + m.z_first;
+                    ptx::mbar_expect_tx(&full[slot], C::SLOT_BYTES);
+                    T* dst = slots + slot * C::SLOT_ELEMS;
 #pragma unroll
-                for (int c = 0; c < C::NBX; ++c) {
-                    if (C::ND == 2)
-                        ptx::tma_load_2d(dst + c * C::CHUNK, &tmap, &full[slot], xs + c * C::BX, zs + sq * C::PB);
-                    else
-                        ptx::tma_load_3d(dst + c * C::CHUNK, &tmap, &full[slot], xs + c * C::BX, ys,
-                                         zs + sq * C::PB);
+                    for (int c = 0; c < C::NBX; ++c) {
+                        if (C::ND == 2)
+                            ptx::tma_load_2d(dst + c * C::CHUNK, &tmap, &full[slot], xs + c * C::BX, zs);
+                        else
+                            ptx::tma_load_3d(dst + c * C::CHUNK, &tmap, &full[slot], xs + c * C::BX, ys, zs);
+                    }
+                }
+            }
+            ++sq;
+            __syncwarp();
+        };
+        // claim the next chunk of this CTA's own segment (contiguous by construction)
+        auto claim = [&](int sg, int* a, int* b) -> bool {
+            int ok = 0, ra = 0, rb = 0;
+            if (lane == 0) {
+                for (;;) {
+                    unsigned long long w;
+                    int nx, en;
+                    seg_state(sc, p.b, sg, &w, &nx, &en);
+                    if (nx >= en) break;
+                    const int nn = min(nx + sc.chunk, en);
+                    if (atomicCAS(&sc.seg[sg], w, seg_pack(sc.epoch, nn, en)) == w) {
+                        ok = 1;
+                        ra = nx;
+                        rb = nn;
+                        break;
+                    }
+                }
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            *a = __shfl_sync(0xffffffffu, ra, 0);
+            *b = __shfl_sync(0xffffffffu, rb, 0);
+            return ok != 0;
+        };
+        // steal the upper half of the largest remaining segment (warp-parallel scan)
+        auto steal = [&](int* vseg, int* a, int* b) -> bool {
+            for (int attempt = 0; attempt < 64; ++attempt) {
+                int best = -1, brem = 0;
+                for (int s = lane; s < sc.nseg; s += 32) {
+                    unsigned long long w;
+                    int nx, en;
+                    seg_state(sc, p.b, s, &w, &nx, &en);
+                    if (en - nx > brem) {
+                        brem = en - nx;
+                        best = s;
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const int r2 = __shfl_xor_sync(0xffffffffu, brem, o);
+                    const int s2 = __shfl_xor_sync(0xffffffffu, best, o);
+                    if (r2 > brem || (r2 == brem && s2 > best)) {
+                        brem = r2;
+                        best = s2;
+                    }
+                }
+                if (best < 0 || brem < sc.min_steal) return false;
+                int ok = 0, ra = 0, rb = 0;
+                if (lane == 0) {
+                    unsigned long long w;
+                    int nx, en;
+                    seg_state(sc, p.b, best, &w, &nx, &en);
+                    const int rem = en - nx;
+                    if (rem >= sc.min_steal) {
+                        const int mid = nx + rem / 2;
+                        if (atomicCAS(&sc.seg[best], w, seg_pack(sc.epoch, nx, mid)) == w) {
+                            ok = 1;
+                            ra = mid;
+                            rb = en;
+                        }
+                    }
+                }
+                ok = __shfl_sync(0xffffffffu, ok, 0);
+                if (ok) {
+                    *vseg = best;
+                    *a = __shfl_sync(0xffffffffu, ra, 0);
+                    *b = __shfl_sync(0xffffffffu, rb, 0);
+                    return true;
+                }
+            }
+            return false;
+        };
+        // take the next never-started segment (grid-stride order) as its owner
+        auto grab = [&](int* s) -> bool {
+            int ok = 0, v = 0;
+            if (lane == 0) {
+                unsigned long long* ctr = &sc.seg[sc.nseg];
+                for (;;) {
+                    const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(ctr);
+                    const unsigned long long cur =
+                        ((unsigned)(w >> 48) == (sc.epoch & 0xFFFFu)) ? (w & 0xFFFFFFFFFFFFull) : gridDim.x;
+                    if (cur >= (unsigned long long)sc.nseg) break;
+                    const unsigned long long nw = ((unsigned long long)(sc.epoch & 0xFFFFu) << 48) | (cur + 1);
+                    if (atomicCAS(ctr, w, nw) == w) {
+                        ok = 1;
+                        v = (int)cur;
+                        break;
+                    }
+                }
+            }
+            ok = __shfl_sync(0xffffffffu, ok, 0);
+            *s = __shfl_sync(0xffffffffu, v, 0);
+            return ok != 0;
+        };
+        if (lane == 0) ptx::prefetch_tmap(&tmap);
+        if (myseg < sc.nseg) {
+            int seg = myseg;   // owned segment (claims are contiguous)
+            int bx, col, lo0, hi0;
+            int a = 0, b = 0;
+            for (;;) {
+                bool own = claim(seg, &a, &b);
+                while (!own && grab(&seg)) own = claim(seg, &a, &b);
+                if (!own) {
+                    int vs;
+                    if (!steal(&vs, &a, &b)) break;
+                    seg_init(p.b, vs, &bx, &col, &lo0, &hi0);
+                } else {
+                    seg_init(p.b, seg, &bx, &col, &lo0, &hi0);
+                }
+                // one run: outputs [run_lo, claimed_hi) of column `col` (planes relative to the box)
+                const int zb = p.b.lo[bx][0];
+                const int run_lo = a;
+                int claimed_hi = b;
+                int z_in = a - C::H;
+                int flags = META_RESTART;
+                for (;;) {
+                    if (own && (claimed_hi + C::H) - (z_in + C::PB) < sc.chunk / 2) {
+                        int ca, cb;
+                        if (claim(seg, &ca, &cb)) claimed_hi = cb;
+                        else own = false;
+                    }
+                    if (z_in > claimed_hi + C::H - 1) break;
+                    put(SlotMeta{zb + z_in, col, zb + run_lo, zb + claimed_hi, flags});
+                    flags = 0;
+                    z_in += C::PB;
                 }
             }
         }
+        put(SlotMeta{0, 0, 0, 0, META_END});
         return;
     }
 
-    // ---- consumers
+    // ================================================================ consumers
     const int tx = threadIdx.x % C::NTX, ty = threadIdx.x / C::NTX;
     int off0[C::NV];
 #pragma unroll
@@ -241,44 +415,57 @@ __global__ void __launch_bounds__(C::NTHREADS)
         off0[v] = (c / C::BX) * C::CHUNK + (c % C::BX);
     }
     Consumer<C> cs;
-#pragma unroll
-    for (int s = 0; s < C::S; ++s)
-#pragma unroll
-        for (int k = 0; k < C::NW; ++k)
-#pragma unroll
-            for (int vy = 0; vy < C::VY; ++vy)
-#pragma unroll
-                for (int vx = 0; vx < C::VX; ++vx) cs.acc[s][k][vy][vx] = T(0);
-
-    // Does this tile's computed extent reach a physical ring (frozen cells)?
-    bool edge = false;
-    if (C::S > 1) {
-        edge |= p.g.phys_lo[0] && (z0 - C::H < 0);
-        edge |= p.g.phys_hi[0] && (z1 + C::H > p.g.n[0]);
-        edge |= p.g.phys_lo[2] && (cx0 - C::PX < 0);
-        edge |= p.g.phys_hi[2] && (cx0 + C::WX + C::PX > p.g.n[2]);
-        if (C::ND == 3) {
-            edge |= p.g.phys_lo[1] && (cy0 - C::RQY < 0);
-            edge |= p.g.phys_hi[1] && (cy0 + C::WY + C::RQY > p.g.n[1]);
-        }
-    }
     const T* __restrict__ src = p.src;
     T* __restrict__ dst = p.dst;
     const long long s0 = p.g.stride0, s1 = p.g.stride1;
-    const int gx = cx0 + tx * C::VX;          // first x of this thread's block
-    const int gy = cy0 + ty * C::VY;          // first y (3D)
-    const int xlo = max(ox0, blo2), xhi = min(ox0 + C::WOX, bhi2);
-    const int ylo = C::ND == 3 ? max(oy0, blo1) : 0, yhi = C::ND == 3 ? min(oy0 + C::WOY, bhi1) : 1;
-
+    int gx = 0, gy = 0, xlo = 0, xhi = 0, ylo = 0, yhi = 0;
+    bool edge_xy = false;
+    int z_first = 0, out_lo = 0, out_hi = 0;
+    bool done = false;
+    int i = 0;
 #pragma unroll 1
-    for (int g = 0; g < NPLP; g += C::NW) {
+    while (!done) {
         auto step = [&](auto PHc) {
             constexpr int PH = decltype(PHc)::value;
-            const int i = g + PH;
-            // ---------------- stage 0: level-0 plane i from the TMA ring
+            if (done) return;
+            const int sq = i / C::PB, pl = i % C::PB, slot = sq % C::NSLOT;
+            if (pl == 0) {
+                ptx::mbar_wait(&full[slot], (sq / C::NSLOT) & 1);
+                const SlotMeta m = meta[slot];
+                if (m.flags & META_END) {
+                    done = true;
+                    return;
+                }
+                if (m.flags & META_RESTART) {
+#pragma unroll
+                    for (int s = 0; s < C::S; ++s)
+#pragma unroll
+                        for (int k = 0; k < C::NW; ++k)
+#pragma unroll
+                            for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                                for (int vx = 0; vx < C::VX; ++vx) cs.acc[s][k][vy][vx] = T(0);
+                    int bx, cx0, cy0;
+                    col_geom(m.col, &bx, &cx0, &cy0, &xlo, &xhi, &ylo, &yhi);
+                    gx = cx0 + tx * C::VX;
+                    gy = cy0 + ty * C::VY;
+                    edge_xy = false;
+                    if (C::S > 1) {
+                        edge_xy |= p.g.phys_lo[2] && (cx0 - C::PX < 0);
+                        edge_xy |= p.g.phys_hi[2] && (cx0 + C::WX + C::PX > p.g.n[2]);
+                        if (C::ND == 3) {
+                            edge_xy |= p.g.phys_lo[1] && (cy0 - C::RQY < 0);
+                            edge_xy |= p.g.phys_hi[1] && (cy0 + C::WY + C::RQY > p.g.n[1]);
+                        }
+                    }
+                }
+                z_first = m.z_first;
+                out_lo = m.out_lo;
+                out_hi = m.out_hi;
+            }
+            const int z_in = z_first + pl;
+            // ---------------- stage 0: level-0 plane from the TMA ring
             {
-                const int sq = i / C::PB, pl = i % C::PB, slot = sq % C::NSLOT;
-                if (pl == 0) ptx::mbar_wait(&full[slot], (sq / C::NSLOT) & 1);
                 const T* base = slots + slot * C::SLOT_ELEMS + (pl * C::ROWS + ty * C::VY) * C::BX;
 #pragma unroll
                 for (int rr = 0; rr < C::NR; ++rr)
@@ -293,17 +480,18 @@ __global__ void __launch_bounds__(C::NTHREADS)
             // ---------------- stages 1..S-1 through shared-memory planes
             auto stage = [&](auto Jc) {
                 constexpr int J = decltype(Jc)::value;
-                constexpr int done = pmod(PH - J * C::RQ, C::NW);
+                constexpr int dn = pmod(PH - J * C::RQ, C::NW);
                 T v[C::VY][C::VX];
 #pragma unroll
                 for (int vy = 0; vy < C::VY; ++vy)
 #pragma unroll
                     for (int vx = 0; vx < C::VX; ++vx) {
-                        v[vy][vx] = cs.acc[J - 1][done][vy][vx];
-                        cs.acc[J - 1][done][vy][vx] = T(0);
+                        v[vy][vx] = cs.acc[J - 1][dn][vy][vx];
+                        cs.acc[J - 1][dn][vy][vx] = T(0);
                     }
-                const int z = z0 - C::H + (i - J * C::RQ);
-                if (edge) {
+                const int z = z_in - J * C::RQ;
+                const bool zface = (p.g.phys_lo[0] && z < 0) || (p.g.phys_hi[0] && z >= p.g.n[0]);
+                if (edge_xy || zface) {
 #pragma unroll
                     for (int vy = 0; vy < C::VY; ++vy)
 #pragma unroll
@@ -343,30 +531,31 @@ __global__ void __launch_bounds__(C::NTHREADS)
             if constexpr (C::S > 2) stage(std::integral_constant<int, 2>{});
             if constexpr (C::S > 3) stage(std::integral_constant<int, 3>{});
             static_assert(C::S <= 4, "at most 4 on-chip stages");
-            // ---------------- output: level-S plane i - H
+            // ---------------- output: level-S plane z_in - H
             {
-                constexpr int done = pmod(PH - C::H, C::NW);
-                const int z = z0 - C::H + (i - C::H);
-                if (z >= z0 && z < z1) {
+                constexpr int dn = pmod(PH - C::H, C::NW);
+                const int z = z_in - C::H;
+                if (z >= out_lo && z < out_hi) {
 #pragma unroll
                     for (int vy = 0; vy < C::VY; ++vy) {
                         const int y = gy + vy;
                         if (y < ylo || y >= yhi) continue;
                         T* op = dst + (p.g.origin[0] + z) * s0 + (p.g.origin[1] + y) * s1 + p.g.origin[2] + gx;
                         if (gx >= xlo && gx + C::VX <= xhi) {
-                            VecT<T>::st(op, cs.acc[C::S - 1][done][vy]);
+                            VecT<T>::st(op, cs.acc[C::S - 1][dn][vy]);
                         } else {
 #pragma unroll
                             for (int vx = 0; vx < C::VX; ++vx)
-                                if (gx + vx >= xlo && gx + vx < xhi) op[vx] = cs.acc[C::S - 1][done][vy][vx];
+                                if (gx + vx >= xlo && gx + vx < xhi) op[vx] = cs.acc[C::S - 1][dn][vy][vx];
                         }
                     }
                 }
 #pragma unroll
                 for (int vy = 0; vy < C::VY; ++vy)
 #pragma unroll
-                    for (int vx = 0; vx < C::VX; ++vx) cs.acc[C::S - 1][done][vy][vx] = T(0);
+                    for (int vx = 0; vx < C::VX; ++vx) cs.acc[C::S - 1][dn][vy][vx] = T(0);
             }
+            ++i;
         };
         [&]<int... PHs>(std::integer_sequence<int, PHs...>) {
             (step(std::integral_constant<int, PHs>{}), ...);
@@ -459,42 +648,60 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
     if ((int)boxes.size() > MAXBOX) return set_error(STENCIL_EUNSUPPORTED, "too many boxes");
     const int occ = occupancy<C>();
     const int target = std::max(1, p->sm_count * occ);
-    int64_t xy_total = 0;
-    std::vector<int> ntx(boxes.size()), nty(boxes.size());
     int64_t vol_total = 0;
+    for (const Box& b : boxes) vol_total += b.volume();
+    prm.b.nbox = (int)boxes.size();
+    int64_t nseg = 0, ncol = 0;
     for (size_t i = 0; i < boxes.size(); ++i) {
         const Box& b = boxes[i];
         int64_t x0 = b.lo[2] - b.lo[2] % C::VX;
-        ntx[i] = (int)((b.hi[2] - x0 + C::WOX - 1) / C::WOX);
-        nty[i] = C::ND == 3 ? (int)((b.hi[1] - b.lo[1] + C::WOY - 1) / C::WOY) : 1;
-        xy_total += (int64_t)ntx[i] * nty[i];
-        vol_total += b.volume();
-    }
-    prm.b.nbox = (int)boxes.size();
-    int64_t tiles = 0;
-    for (size_t i = 0; i < boxes.size(); ++i) {
-        const Box& b = boxes[i];
-        int64_t zlen = b.hi[0] - b.lo[0];
-        int64_t xy = (int64_t)ntx[i] * nty[i];
-        // chunks so that the whole launch is about one wave of resident CTAs
+        const int ntx = (int)((b.hi[2] - x0 + C::WOX - 1) / C::WOX);
+        const int nty = C::ND == 3 ? (int)((b.hi[1] - b.lo[1] + C::WOY - 1) / C::WOY) : 1;
+        const int64_t zlen = b.hi[0] - b.lo[0];
+        const int64_t cols = (int64_t)ntx * nty;
+        // initial segments: about one resident wave of CTAs, split by volume
         double share = vol_total > 0 ? double(b.volume()) / double(vol_total) : 1.0;
-        int64_t want = std::max<int64_t>(1, (int64_t)(target * share) / std::max<int64_t>(1, xy));
-        int64_t minlen = std::max<int64_t>(8, 4 * C::H);
-        int64_t nch = std::min<int64_t>(want, std::max<int64_t>(1, zlen / minlen));
+        int64_t want = std::max<int64_t>(1, (int64_t)(target * share) / std::max<int64_t>(1, cols));
+        int64_t nch = std::min<int64_t>(want, std::max<int64_t>(1, zlen / 8));
         int64_t zc = (zlen + nch - 1) / nch;
         nch = (zlen + zc - 1) / zc;
         for (int a = 0; a < 3; ++a) {
             prm.b.lo[i][a] = (int)b.lo[a];
             prm.b.hi[i][a] = (int)b.hi[a];
         }
-        prm.b.tx[i] = ntx[i];
-        prm.b.ty[i] = nty[i];
+        prm.b.tx[i] = ntx;
+        prm.b.ty[i] = nty;
         prm.b.zchunk[i] = (int)zc;
-        prm.b.tiles_begin[i] = (int)tiles;
-        tiles += xy * nch;
+        prm.b.seg_begin[i] = (int)nseg;
+        prm.b.col_begin[i] = (int)ncol;
+        nseg += cols * nch;
+        ncol += cols;
     }
-    prm.b.tiles_begin[boxes.size()] = (int)tiles;
-    (void)xy_total;
+    prm.b.seg_begin[boxes.size()] = (int)nseg;
+    prm.b.col_begin[boxes.size()] = (int)ncol;
+    // dynamic-schedule scratch + epoch
+    if (p->sched_words < nseg + 1) {
+        if (p->sched) cudaFree(p->sched);
+        p->sched = nullptr;
+        int64_t words = std::max<int64_t>(nseg + 1, 8192);
+        cudaError_t e = cudaMalloc(&p->sched, words * 8);
+        if (e != cudaSuccess) return cuda_error(e, "cudaMalloc(schedule scratch)");
+        e = cudaMemsetAsync(p->sched, 0, words * 8, (cudaStream_t)c.stream);
+        if (e != cudaSuccess) return cuda_error(e, "cudaMemsetAsync");
+        p->sched_words = words;
+        p->epoch = 0;
+    }
+    p->epoch = (p->epoch + 1) & 0xFFFFu;
+    if (p->epoch == 0) {
+        cudaMemsetAsync(p->sched, 0, p->sched_words * 8, (cudaStream_t)c.stream);
+        p->epoch = 1;
+    }
+    prm.sc.seg = static_cast<unsigned long long*>(p->sched);
+    prm.sc.epoch = p->epoch;
+    prm.sc.nseg = (int)nseg;
+    prm.sc.chunk = std::max(2 * C::PB, 16);
+    prm.sc.min_steal = std::max(2 * prm.sc.chunk, 4 * C::H + 8);
+    const int64_t tiles = std::min<int64_t>(nseg, target);   // persistent: one resident wave
     CUtensorMap map;
     int rc = make_tmap<C>(L, c.src, &map);
     if (rc) return rc;

@@ -16,12 +16,26 @@ struct DevGeom {
     int ext[3];
 };
 
+// Output boxes of one launch, tiled into columns (in-plane tiles streamed
+// along axis 0) and, initially, `parts` equal z-segments per column.
 struct DevBoxes {
     int nbox;
     int lo[MAXBOX][3], hi[MAXBOX][3];
-    int tiles_begin[MAXBOX + 1];
-    int tx[MAXBOX], ty[MAXBOX];
-    int zchunk[MAXBOX];
+    int seg_begin[MAXBOX + 1];   // first segment of each box
+    int col_begin[MAXBOX + 1];   // first global column id of each box
+    int tx[MAXBOX], ty[MAXBOX];  // columns per box along x and y
+    int zchunk[MAXBOX];          // initial segment length (planes)
+};
+
+// Dynamic schedule: one 64-bit word per segment (epoch | next | end) in a
+// plan-owned device scratch; CTAs claim contiguous chunks of their own segment
+// and steal the upper half of the largest remaining segment when done.
+struct DevSched {
+    unsigned long long* seg;
+    unsigned int epoch;
+    int nseg;
+    int chunk;
+    int min_steal;
 };
 
 template <typename T, int NC>
@@ -30,6 +44,7 @@ struct SweepParams {
     T* dst;
     DevGeom g;
     DevBoxes b;
+    DevSched sc;
     T coef[NC];
 };
 
