@@ -1,4 +1,4 @@
-// aux.cu — the boundary band (K-G3), the 1D on-chip multi-step kernel (K-G4),
+// aux.cu — the 1D on-chip multi-step kernel (K-G4),
 // the frozen-ring initialisation (K-G5) and the seeded field generator (K-G0).
 #include <cuda_runtime.h>
 
@@ -12,197 +12,6 @@ namespace sb {
 
 int cuda_error(int e, const char* what) {
     return set_error(STENCIL_ECUDA, std::string(what) + ": " + cudaGetErrorString((cudaError_t)e));
-}
-
-// ============================================================== K-G3 band
-// Points within (m-1)*r of a FIXED face: the folded weights are invalid there
-// (R2), so they get the exact result of m single steps.  Each CTA
-// loads its output block plus an m*r halo into shared memory and runs m
-// single steps of the ORIGINAL taps on a shrinking region; cells of the
-// physical ring keep u0 at every step (R1).
-constexpr int BAND_MAXT = 125;
-constexpr int BAND_MAXBOX = 26;
-constexpr int BAND_THREADS = 256;
-
-template <typename T>
-struct BandParams {
-    const T* src;
-    T* dst;
-    DevGeom g;
-    int nbox;
-    int lo[BAND_MAXBOX][3], hi[BAND_MAXBOX][3];
-    int blk[BAND_MAXBOX][3];        // output block extents
-    int nblk[BAND_MAXBOX][3];       // blocks per axis
-    int begin[BAND_MAXBOX + 1];
-    int m, r, ntaps;
-    int used[3];                    // axis carries a stencil extent
-    int toff[BAND_MAXT][3];
-    T w[BAND_MAXT];
-};
-
-template <typename T>
-__global__ void __launch_bounds__(BAND_THREADS) band_kernel(const __grid_constant__ BandParams<T> p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    T* buf0 = reinterpret_cast<T*>(smem_raw);
-    int bid = blockIdx.x, b = 0;
-    while (b + 1 < p.nbox && bid >= p.begin[b + 1]) ++b;
-    int t = bid - p.begin[b];
-    int bi[3];
-    bi[2] = t % p.nblk[b][2];
-    t /= p.nblk[b][2];
-    bi[1] = t % p.nblk[b][1];
-    bi[0] = t / p.nblk[b][1];
-    int olo[3], ohi[3], ilo[3], ie[3], H[3];
-    for (int a = 0; a < 3; ++a) {
-        olo[a] = p.lo[b][a] + bi[a] * p.blk[b][a];
-        ohi[a] = min(olo[a] + p.blk[b][a], p.hi[b][a]);
-        H[a] = p.used[a] ? p.m * p.r : 0;
-        ilo[a] = olo[a] - H[a];
-        ie[a] = ohi[a] - olo[a] + 2 * H[a];
-    }
-    const int vol = ie[0] * ie[1] * ie[2];
-    T* buf1 = buf0 + vol;
-    const long long s0 = p.g.stride0, s1 = p.g.stride1;
-    // load input block (cells outside the allocation -> 0; never used by valid outputs)
-    for (int e = threadIdx.x; e < vol; e += blockDim.x) {
-        int c2 = e % ie[2], c1 = (e / ie[2]) % ie[1], c0 = e / (ie[2] * ie[1]);
-        long long g0 = p.g.origin[0] + ilo[0] + c0, g1 = p.g.origin[1] + ilo[1] + c1,
-                  g2 = p.g.origin[2] + ilo[2] + c2;
-        T v = T(0);
-        if (g0 >= 0 && g0 < p.g.ext[0] && g1 >= 0 && g1 < p.g.ext[1] && g2 >= 0 && g2 < p.g.ext[2])
-            v = p.src[g0 * s0 + g1 * s1 + g2];
-        buf0[e] = v;
-    }
-    __syncthreads();
-    int loff[BAND_MAXT];
-    for (int j = 0; j < p.ntaps; ++j) loff[j] = (p.toff[j][0] * ie[1] + p.toff[j][1]) * ie[2] + p.toff[j][2];
-    T* cur = buf0;
-    T* nxt = buf1;
-    for (int s = 1; s <= p.m; ++s) {
-        int rlo[3], re[3];
-        for (int a = 0; a < 3; ++a) {
-            int sh = p.used[a] ? s * p.r : 0;
-            rlo[a] = sh;
-            re[a] = ie[a] - 2 * sh;
-        }
-        const int rvol = re[0] * re[1] * re[2];
-        for (int e = threadIdx.x; e < rvol; e += blockDim.x) {
-            int c2 = e % re[2] + rlo[2], c1 = (e / re[2]) % re[1] + rlo[1], c0 = e / (re[2] * re[1]) + rlo[0];
-            int q[3] = {ilo[0] + c0, ilo[1] + c1, ilo[2] + c2};
-            bool ring = false;
-            for (int a = 0; a < 3; ++a) {
-                if (!p.used[a]) continue;
-                if ((q[a] < 0 && p.g.phys_lo[a]) || (q[a] >= p.g.n[a] && p.g.phys_hi[a])) ring = true;
-            }
-            int li = (c0 * ie[1] + c1) * ie[2] + c2;
-            T acc;
-            if (ring) {
-                acc = cur[li];
-            } else {
-                acc = T(0);
-                for (int j = 0; j < p.ntaps; ++j) acc = fma(p.w[j], cur[li + loff[j]], acc);
-            }
-            nxt[li] = acc;
-        }
-        __syncthreads();
-        T* tmp = cur;
-        cur = nxt;
-        nxt = tmp;
-    }
-    const int ovol = (ohi[0] - olo[0]) * (ohi[1] - olo[1]) * (ohi[2] - olo[2]);
-    const int oe1 = ohi[1] - olo[1], oe2 = ohi[2] - olo[2];
-    for (int e = threadIdx.x; e < ovol; e += blockDim.x) {
-        int c2 = e % oe2, c1 = (e / oe2) % oe1, c0 = e / (oe2 * oe1);
-        int li = ((c0 + H[0]) * ie[1] + (c1 + H[1])) * ie[2] + (c2 + H[2]);
-        p.dst[(p.g.origin[0] + olo[0] + c0) * s0 + (p.g.origin[1] + olo[1] + c1) * s1 + p.g.origin[2] + olo[2] +
-              c2] = cur[li];
-    }
-}
-
-template <typename T>
-static int launch_band_t(Plan* p, const BandCall& c) {
-    const Layout3& L = *c.L;
-    BandParams<T> prm;
-    std::memset(&prm, 0, sizeof(prm));
-    prm.src = static_cast<const T*>(c.src);
-    prm.dst = static_cast<T*>(c.dst);
-    fill_geom(L, &prm.g);
-    prm.m = c.m;
-    prm.r = p->r;
-    int nd = p->ndim;
-    prm.used[0] = nd >= 2;
-    prm.used[1] = nd == 3;
-    prm.used[2] = 1;
-    int k = (int)p->w.size();
-    if (k > BAND_MAXT) return set_error(STENCIL_EUNSUPPORTED, "too many taps for the band kernel");
-    prm.ntaps = k;
-    for (int j = 0; j < k; ++j) {
-        int o3[3] = {0, 0, 0};
-        if (nd == 1) o3[2] = p->taps[j];
-        if (nd == 2) { o3[0] = p->taps[j * 2]; o3[2] = p->taps[j * 2 + 1]; }
-        if (nd == 3) { o3[0] = p->taps[j * 3]; o3[1] = p->taps[j * 3 + 1]; o3[2] = p->taps[j * 3 + 2]; }
-        for (int a = 0; a < 3; ++a) prm.toff[j][a] = o3[a];
-        prm.w[j] = static_cast<T>(p->w[j]);
-    }
-    const int H = c.m * p->r;
-    const size_t smem_cap = 96 * 1024;
-    int nb = 0;
-    int64_t total = 0;
-    for (const Box& b : c.boxes) {
-        if (b.empty()) continue;
-        if (nb >= BAND_MAXBOX) return set_error(STENCIL_EUNSUPPORTED, "too many band boxes");
-        int blk[3];
-        for (int a = 0; a < 3; ++a) {
-            int64_t e = b.hi[a] - b.lo[a];
-            int cap = (nd == 3) ? 16 : (a == 2 ? 256 : 32);
-            blk[a] = (int)std::min<int64_t>(e, cap);
-        }
-        // shrink until two buffers fit
-        for (;;) {
-            size_t vol = 1;
-            for (int a = 0; a < 3; ++a) vol *= (size_t)(blk[a] + (prm.used[a] ? 2 * H : 0));
-            if (2 * vol * sizeof(T) <= smem_cap) break;
-            int am = 0;
-            for (int a = 1; a < 3; ++a)
-                if (blk[a] > blk[am]) am = a;
-            if (blk[am] <= 1) return set_error(STENCIL_EUNSUPPORTED, "band halo too large");
-            blk[am] = (blk[am] + 1) / 2;
-        }
-        prm.begin[nb] = (int)total;
-        int64_t cnt = 1;
-        for (int a = 0; a < 3; ++a) {
-            prm.lo[nb][a] = (int)b.lo[a];
-            prm.hi[nb][a] = (int)b.hi[a];
-            prm.blk[nb][a] = blk[a];
-            prm.nblk[nb][a] = (int)((b.hi[a] - b.lo[a] + blk[a] - 1) / blk[a]);
-            cnt *= prm.nblk[nb][a];
-        }
-        total += cnt;
-        ++nb;
-    }
-    if (nb == 0) return 0;
-    prm.nbox = nb;
-    prm.begin[nb] = (int)total;
-    size_t smem = 0;
-    for (int i = 0; i < nb; ++i) {
-        size_t vol = 1;
-        for (int a = 0; a < 3; ++a) vol *= (size_t)(prm.blk[i][a] + (prm.used[a] ? 2 * H : 0));
-        smem = std::max(smem, 2 * vol * sizeof(T));
-    }
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[sizeof(T) == 8]) {
-        cudaFuncSetAttribute(band_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_cap);
-        attr_set[sizeof(T) == 8] = true;
-    }
-    band_kernel<T><<<(unsigned)total, BAND_THREADS, smem, (cudaStream_t)c.stream>>>(prm);
-    cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return cuda_error(e, "band_kernel launch");
-    return 1;
-}
-
-int launch_band(Plan* p, const BandCall& c) {
-    if (c.m <= 1) return 0;
-    return p->dtype == STENCIL_F64 ? launch_band_t<double>(p, c) : launch_band_t<float>(p, c);
 }
 
 // ============================================================== K-G4 1D

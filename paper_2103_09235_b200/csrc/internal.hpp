@@ -88,20 +88,11 @@ struct SweepCall {
     std::vector<Box> boxes;   // output boxes (interior coords)
     int q, stages;
     const std::vector<double>* coef;   // lambda^(q), dense fp64
+    std::vector<Box> band;    // exact stepwise band boxes (K-G3), same launch
+    int band_m = 1;           // steps of the band (the sweep's fold_m)
     void* stream;
 };
 int launch_sweep(Plan* p, const SweepCall& c);
-
-// Exact stepwise m-step band over boxes (K-G3).
-struct BandCall {
-    const void* src;
-    void* dst;
-    const Layout3* L;
-    std::vector<Box> boxes;
-    int m;
-    void* stream;
-};
-int launch_band(Plan* p, const BandCall& c);
 
 // 1D on-chip multi-step kernel (K-G4): T steps (fold m) in one launch.
 int launch_1d(Plan* p, const void* src, void* dst, const Layout3* L, int64_t T, int m,

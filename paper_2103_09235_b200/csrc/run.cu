@@ -110,33 +110,24 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
     sc.stages = s.v.stages;
     sc.coef = &folded(p, s.v.q);
     sc.stream = stream;
+    if (s.m > 1) {
+        for (const Box& b : band) {
+            Box c = clip0(b, z0, z1);
+            if (!c.empty()) sc.band.push_back(c);
+        }
+        sc.band_m = s.m;
+    }
     int rc;
     {
-        const int64_t pts = mb.volume();
-        TimedScope ts(p, stream, 0, 2 * L.esize * pts,
-                      pts * s.v.stages * support_size(p->ndim, p->shape, p->r, s.v.q));
+        int64_t pts = mb.volume(), bpts = 0;
+        for (const Box& b : sc.band) bpts += b.volume();
+        TimedScope ts(p, stream, 0, 2 * L.esize * (pts + bpts),
+                      pts * s.v.stages * support_size(p->ndim, p->shape, p->r, s.v.q) +
+                          bpts * s.m * (int64_t)p->w.size());
         rc = launch_sweep(p, sc);
     }
     if (rc < 0) return rc;
     launches += rc;
-    if (s.m > 1) {
-        BandCall bc;
-        bc.src = src;
-        bc.dst = dst;
-        bc.L = &L;
-        for (const Box& b : band) {
-            Box c = clip0(b, z0, z1);
-            if (!c.empty()) bc.boxes.push_back(c);
-        }
-        bc.m = s.m;
-        bc.stream = stream;
-        int64_t pts = 0;
-        for (const Box& b : bc.boxes) pts += b.volume();
-        TimedScope ts(p, stream, 1, 2 * L.esize * pts, pts * s.m * (int64_t)p->w.size());
-        rc = launch_band(p, bc);
-        if (rc < 0) return rc;
-        launches += rc;
-    }
     return launches;
 }
 

@@ -78,6 +78,8 @@ struct Cfg {
     static constexpr int NCW = NCONS / 32;
     static constexpr int NTHREADS = NCONS + 32;
     static constexpr int NC = ND == 3 ? NW * NW * NW : NW * NW;
+    static constexpr size_t DATA_BYTES = (size_t)NSLOT * SLOT_ELEMS * sizeof(T) +
+                                         (size_t)(S - 1) * 2 * LEV_ELEMS * sizeof(T);
     static constexpr size_t SMEM = (size_t)NSLOT * SLOT_ELEMS * sizeof(T) +
                                    (size_t)(S - 1) * 2 * LEV_ELEMS * sizeof(T) + 2 * NSLOT * 8 + NSLOT * 32;
     static_assert(NCONS % 32 == 0, "consumer threads must be whole warps");
@@ -161,6 +163,90 @@ struct Consumer {
     }
 };
 
+// ------------------------------------------------------------------ K-G3 band
+// One band block: load the output block plus an m*r halo (clipped at FIXED
+// faces to the r-wide ring: nothing beyond the ring is ever needed), run m
+// single steps of the ORIGINAL taps on the shrinking region, ring cells
+// frozen at u0 (R1/R2), store the block.
+template <typename T>
+__device__ __forceinline__ void band_block(const BandDesc<T>& bd, const DevGeom& g, const T* __restrict__ src,
+                                        T* __restrict__ dst, int blk_id, T* smem, int tid, int nthr) {
+    int b = 0;
+    while (b + 1 < bd.nbox && blk_id >= bd.begin[b + 1]) ++b;
+    int t = blk_id - bd.begin[b];
+    int bi[3];
+    bi[2] = t % bd.nblk[b][2];
+    t /= bd.nblk[b][2];
+    bi[1] = t % bd.nblk[b][1];
+    bi[0] = t / bd.nblk[b][1];
+    int olo[3], ohi[3], ilo[3], ie[3], clo[3], chi[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        olo[a] = bd.lo[b][a] + bi[a] * bd.blk[b][a];
+        ohi[a] = min(olo[a] + bd.blk[b][a], bd.hi[b][a]);
+        const int H = bd.used[a] ? bd.m * bd.r : 0;
+        int lo = olo[a] - H, hi = ohi[a] + H;
+        clo[a] = bd.used[a] && g.phys_lo[a] && lo < -bd.r;
+        chi[a] = bd.used[a] && g.phys_hi[a] && hi > g.n[a] + bd.r;
+        if (clo[a]) lo = -bd.r;
+        if (chi[a]) hi = g.n[a] + bd.r;
+        ilo[a] = lo;
+        ie[a] = hi - lo;
+    }
+    const int vol = ie[0] * ie[1] * ie[2];
+    T* cur = smem;
+    T* nxt = smem + vol;
+    const long long s0 = g.stride0, s1 = g.stride1;
+    for (int e = tid; e < vol; e += nthr) {
+        const int c2 = e % ie[2], c1 = (e / ie[2]) % ie[1], c0 = e / (ie[2] * ie[1]);
+        const long long a0 = g.origin[0] + ilo[0] + c0, a1 = g.origin[1] + ilo[1] + c1, a2 = g.origin[2] + ilo[2] + c2;
+        T v = T(0);
+        if (a0 >= 0 && a0 < g.ext[0] && a1 >= 0 && a1 < g.ext[1] && a2 >= 0 && a2 < g.ext[2]) v = src[a0 * s0 + a1 * s1 + a2];
+        cur[e] = v;
+    }
+    __syncthreads();
+    for (int s = 1; s <= bd.m; ++s) {
+        int rlo[3], re[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int sh = bd.used[a] ? s * bd.r : 0;
+            rlo[a] = clo[a] ? 0 : sh;
+            re[a] = ie[a] - rlo[a] - (chi[a] ? 0 : sh);
+        }
+        const int rvol = re[0] * re[1] * re[2];
+        for (int e = tid; e < rvol; e += nthr) {
+            const int c2 = e % re[2] + rlo[2], c1 = (e / re[2]) % re[1] + rlo[1], c0 = e / (re[2] * re[1]) + rlo[0];
+            const int q[3] = {ilo[0] + c0, ilo[1] + c1, ilo[2] + c2};
+            bool ring = false;
+#pragma unroll
+            for (int a = 0; a < 3; ++a)
+                if (bd.used[a] && ((q[a] < 0 && g.phys_lo[a]) || (q[a] >= g.n[a] && g.phys_hi[a]))) ring = true;
+            const int li = (c0 * ie[1] + c1) * ie[2] + c2;
+            T acc;
+            if (ring) {
+                acc = cur[li];
+            } else {
+                acc = T(0);
+                for (int j = 0; j < bd.ntaps; ++j)
+                    acc = fmaT(bd.w[j], cur[li + (bd.toff[j][0] * ie[1] + bd.toff[j][1]) * ie[2] + bd.toff[j][2]], acc);
+            }
+            nxt[li] = acc;
+        }
+        __syncthreads();
+        T* tmp = cur;
+        cur = nxt;
+        nxt = tmp;
+    }
+    const int oe1 = ohi[1] - olo[1], oe2 = ohi[2] - olo[2];
+    const int ovol = (ohi[0] - olo[0]) * oe1 * oe2;
+    for (int e = tid; e < ovol; e += nthr) {
+        const int c2 = e % oe2, c1 = (e / oe2) % oe1, c0 = e / (oe2 * oe1);
+        const int li = ((olo[0] - ilo[0] + c0) * ie[1] + (olo[1] - ilo[1] + c1)) * ie[2] + (olo[2] - ilo[2] + c2);
+        dst[(g.origin[0] + olo[0] + c0) * s0 + (g.origin[1] + olo[1] + c1) * s1 + g.origin[2] + olo[2] + c2] = cur[li];
+    }
+    __syncthreads();
+}
+
 // Per-slot metadata written by the producer before the slot's TMA is issued
 // (ordered by the mbarrier's release/acquire), read by the consumers.
 struct SlotMeta {
@@ -216,6 +302,10 @@ __global__ void __launch_bounds__(C::NTHREADS)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+            p.sc.ctr[((p.sc.epoch + 1) & 1) * 2 + 0] = 0u;
+            p.sc.ctr[((p.sc.epoch + 1) & 1) * 2 + 1] = 0u;
+        }
 #pragma unroll
         for (int s = 0; s < C::NSLOT; ++s) {
             ptx::mbar_init(&full[s], 1);
@@ -348,25 +438,11 @@ __global__ void __launch_bounds__(C::NTHREADS)
         };
         // take the next never-started segment (grid-stride order) as its owner
         auto grab = [&](int* s) -> bool {
-            int ok = 0, v = 0;
-            if (lane == 0) {
-                unsigned long long* ctr = &sc.seg[sc.nseg];
-                for (;;) {
-                    const unsigned long long w = *reinterpret_cast<volatile unsigned long long*>(ctr);
-                    const unsigned long long cur =
-                        ((unsigned)(w >> 48) == (sc.epoch & 0xFFFFu)) ? (w & 0xFFFFFFFFFFFFull) : gridDim.x;
-                    if (cur >= (unsigned long long)sc.nseg) break;
-                    const unsigned long long nw = ((unsigned long long)(sc.epoch & 0xFFFFu) << 48) | (cur + 1);
-                    if (atomicCAS(ctr, w, nw) == w) {
-                        ok = 1;
-                        v = (int)cur;
-                        break;
-                    }
-                }
-            }
-            ok = __shfl_sync(0xffffffffu, ok, 0);
-            *s = __shfl_sync(0xffffffffu, v, 0);
-            return ok != 0;
+            int v = 0;
+            if (lane == 0) v = (int)atomicAdd(&sc.ctr[(sc.epoch & 1) * 2 + 0], 1u) + (int)gridDim.x;
+            v = __shfl_sync(0xffffffffu, v, 0);
+            *s = v;
+            return v < sc.nseg;
         };
         if (lane == 0) ptx::prefetch_tmap(&tmap);
         if (myseg < sc.nseg) {
@@ -403,8 +479,7 @@ __global__ void __launch_bounds__(C::NTHREADS)
             }
         }
         put(SlotMeta{0, 0, 0, 0, META_END});
-        return;
-    }
+    } else {
 
     // ================================================================ consumers
     const int tx = threadIdx.x % C::NTX, ty = threadIdx.x / C::NTX;
@@ -561,6 +636,20 @@ __global__ void __launch_bounds__(C::NTHREADS)
             (step(std::integral_constant<int, PHs>{}), ...);
         }(std::make_integer_sequence<int, C::NW>{});
     }
+    }  // consumers
+
+    // ================================================================ band (tail filler)
+    if (p.band.nblk_total > 0) {
+        __shared__ int s_blk;
+        __syncthreads();
+        for (;;) {
+            if (threadIdx.x == 0) s_blk = (int)atomicAdd(&p.sc.ctr[(p.sc.epoch & 1) * 2 + 1], 1u);
+            __syncthreads();
+            const int blk = s_blk;
+            if (blk >= p.band.nblk_total) break;
+            band_block<T>(p.band, p.g, p.src, p.dst, blk, slots, threadIdx.x, C::NTHREADS);
+        }
+    }
 }
 
 // ------------------------------------------------------------------ host side
@@ -629,6 +718,66 @@ static int occupancy() {
     return occ;
 }
 
+// Cut the band boxes into blocks whose two shared-memory buffers fit in the
+// sweep kernel's data region.
+template <typename T>
+static int plan_band(Plan* p, const SweepCall& c, BandDesc<T>* bd, size_t smem_cap, int64_t* nblk_total) {
+    const int nd = p->ndim;
+    bd->m = c.band_m;
+    bd->r = p->r;
+    bd->used[0] = nd >= 2;
+    bd->used[1] = nd == 3;
+    bd->used[2] = 1;
+    const int k = (int)p->w.size();
+    if (k > BAND_MAXT) return set_error(STENCIL_EUNSUPPORTED, "too many taps for the band");
+    bd->ntaps = k;
+    for (int j = 0; j < k; ++j) {
+        int o3[3] = {0, 0, 0};
+        if (nd == 1) o3[2] = p->taps[j];
+        if (nd == 2) { o3[0] = p->taps[j * 2]; o3[2] = p->taps[j * 2 + 1]; }
+        if (nd == 3) { o3[0] = p->taps[j * 3]; o3[1] = p->taps[j * 3 + 1]; o3[2] = p->taps[j * 3 + 2]; }
+        for (int a = 0; a < 3; ++a) bd->toff[j][a] = (short)o3[a];
+        bd->w[j] = static_cast<T>(p->w[j]);
+    }
+    const int H = c.band_m * p->r;
+    int nb = 0;
+    int64_t total = 0;
+    for (const Box& b : c.band) {
+        if (b.empty()) continue;
+        if (nb >= BAND_MAXBOX) return set_error(STENCIL_EUNSUPPORTED, "too many band boxes");
+        int blk[3];
+        const int cap[3] = {nd == 3 ? 64 : 64, 64, nd == 3 ? 64 : 256};
+        for (int a = 0; a < 3; ++a) blk[a] = (int)std::min<int64_t>(b.hi[a] - b.lo[a], cap[a]);
+        for (;;) {
+            size_t vol = 1;
+            for (int a = 0; a < 3; ++a) vol *= (size_t)(blk[a] + (bd->used[a] ? 2 * H : 0));
+            if (2 * vol * sizeof(T) <= smem_cap) break;
+            // shrink the largest axis, keeping x (coalescing) longest when tied
+            int am = 2;
+            for (int a = 1; a >= 0; --a)
+                if (blk[a] > blk[am] || (blk[a] == blk[am] && a < am && blk[a] > 1)) am = a;
+            if (blk[am] <= 1) return set_error(STENCIL_EUNSUPPORTED, "band halo too large for the tile");
+            blk[am] = (blk[am] + 1) / 2;
+        }
+        bd->begin[nb] = (int)total;
+        int64_t cnt = 1;
+        for (int a = 0; a < 3; ++a) {
+            bd->lo[nb][a] = (int)b.lo[a];
+            bd->hi[nb][a] = (int)b.hi[a];
+            bd->blk[nb][a] = blk[a];
+            bd->nblk[nb][a] = (int)((b.hi[a] - b.lo[a] + blk[a] - 1) / blk[a]);
+            cnt *= bd->nblk[nb][a];
+        }
+        total += cnt;
+        ++nb;
+    }
+    bd->nbox = nb;
+    bd->begin[nb] = (int)total;
+    bd->nblk_total = (int)total;
+    *nblk_total = total;
+    return STENCIL_OK;
+}
+
 template <class C>
 static int launch_cfg(Plan* p, const SweepCall& c) {
     using T = typename C::T;
@@ -644,7 +793,12 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
     std::vector<Box> boxes;
     for (const Box& b : c.boxes)
         if (!b.empty()) boxes.push_back(b);
-    if (boxes.empty()) return 0;
+    int64_t band_blocks = 0;
+    if (c.band_m > 1) {
+        int rc = plan_band<T>(p, c, &prm.band, C::DATA_BYTES, &band_blocks);
+        if (rc) return rc;
+    }
+    if (boxes.empty() && band_blocks == 0) return 0;
     if ((int)boxes.size() > MAXBOX) return set_error(STENCIL_EUNSUPPORTED, "too many boxes");
     const int occ = occupancy<C>();
     const int target = std::max(1, p->sm_count * occ);
@@ -679,11 +833,16 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
     }
     prm.b.seg_begin[boxes.size()] = (int)nseg;
     prm.b.col_begin[boxes.size()] = (int)ncol;
-    // dynamic-schedule scratch + epoch
-    if (p->sched_words < nseg + 1) {
+    CUtensorMap map;
+    {
+        int rc = make_tmap<C>(L, c.src, &map);
+        if (rc) return rc;
+    }
+    // dynamic-schedule scratch + epoch (advanced only for a launch that happens)
+    if (p->sched_words < nseg + 4) {
         if (p->sched) cudaFree(p->sched);
         p->sched = nullptr;
-        int64_t words = std::max<int64_t>(nseg + 1, 8192);
+        int64_t words = std::max<int64_t>(nseg + 4, 8192);
         cudaError_t e = cudaMalloc(&p->sched, words * 8);
         if (e != cudaSuccess) return cuda_error(e, "cudaMalloc(schedule scratch)");
         e = cudaMemsetAsync(p->sched, 0, words * 8, (cudaStream_t)c.stream);
@@ -697,14 +856,13 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
         p->epoch = 1;
     }
     prm.sc.seg = static_cast<unsigned long long*>(p->sched);
+    prm.sc.ctr = reinterpret_cast<unsigned int*>(static_cast<unsigned long long*>(p->sched) + p->sched_words - 2);
     prm.sc.epoch = p->epoch;
     prm.sc.nseg = (int)nseg;
     prm.sc.chunk = std::max(2 * C::PB, 16);
     prm.sc.min_steal = std::max(2 * prm.sc.chunk, 4 * C::H + 8);
-    const int64_t tiles = std::min<int64_t>(nseg, target);   // persistent: one resident wave
-    CUtensorMap map;
-    int rc = make_tmap<C>(L, c.src, &map);
-    if (rc) return rc;
+    int64_t tiles = std::min<int64_t>(nseg, target);   // persistent: one resident wave
+    if (band_blocks > 0) tiles = std::max<int64_t>(tiles, std::min<int64_t>(band_blocks, target));
     sweep_kernel<C><<<(unsigned)tiles, C::NTHREADS, C::SMEM, (cudaStream_t)c.stream>>>(map, prm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "sweep_kernel launch");

@@ -32,10 +32,30 @@ struct DevBoxes {
 // and steal the upper half of the largest remaining segment when done.
 struct DevSched {
     unsigned long long* seg;
+    unsigned int* ctr;        // [2 parities][2]: grab counter, band counter (this launch: epoch & 1)
     unsigned int epoch;
     int nseg;
     int chunk;
     int min_steal;
+};
+
+// The exact stepwise band (K-G3) carried by the same launch: boxes within
+// (m-1)*r of a FIXED face, cut into blocks that CTAs claim once their main
+// work is exhausted (the band fills the tail of the sweep).
+constexpr int BAND_MAXT = 125;
+constexpr int BAND_MAXBOX = 26;
+
+template <typename T>
+struct BandDesc {
+    int nbox, nblk_total;
+    int lo[BAND_MAXBOX][3], hi[BAND_MAXBOX][3];
+    int blk[BAND_MAXBOX][3];
+    int nblk[BAND_MAXBOX][3];
+    int begin[BAND_MAXBOX + 1];
+    int m, r, ntaps;
+    int used[3];
+    short toff[BAND_MAXT][3];
+    T w[BAND_MAXT];
 };
 
 template <typename T, int NC>
@@ -45,6 +65,7 @@ struct SweepParams {
     DevGeom g;
     DevBoxes b;
     DevSched sc;
+    BandDesc<T> band;
     T coef[NC];
 };
 
