@@ -73,6 +73,12 @@ def _load():
                 ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double), ctypes.c_int,
                 ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.POINTER(ctypes.c_double),
                 ctypes.c_int]
+            lib.oracle_run_cone.restype = ctypes.c_int
+            lib.oracle_run_cone.argtypes = [
+                ctypes.c_int, ctypes.POINTER(ctypes.c_int64), ctypes.c_int, ctypes.c_int,
+                ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_double),
+                ctypes.POINTER(ctypes.c_double), ctypes.c_int64, ctypes.POINTER(ctypes.c_int64),
+                ctypes.POINTER(ctypes.c_int64), ctypes.POINTER(ctypes.c_double), ctypes.c_int]
             lib.oracle_max_threads.restype = ctypes.c_int
             _lib = lib
     return _lib
@@ -163,13 +169,41 @@ def window_for(dims, r: int, T: int, lo, hi):
     return wlo, whi
 
 
-def run_window(dims, r: int, offs, w, T: int, lo, hi, u0_block_fn, nthreads: int = 0):
+def run_cone(dims, r: int, offs, w, u0: np.ndarray, T: int, blo, bhi, nthreads: int = 0) -> np.ndarray:
+    """T FIXED steps updating, at step t, only the points within (T-t) r of the
+    interior box [blo, bhi): the box's values equal a full run's bit for bit."""
+    lib = _load()
+    nd = len(dims)
+    u0 = np.ascontiguousarray(u0, dtype=np.float64)
+    out = np.empty_like(u0)
+    d = (ctypes.c_int64 * nd)(*[int(n) for n in dims])
+    flat = [int(c) for o in offs for c in o]
+    o_arr = (ctypes.c_int * len(flat))(*flat)
+    w_arr = np.ascontiguousarray(w, dtype=np.float64)
+    lo = (ctypes.c_int64 * nd)(*[int(v) for v in blo])
+    hi = (ctypes.c_int64 * nd)(*[int(v) for v in bhi])
+    rc = lib.oracle_run_cone(nd, d, int(r), len(offs), o_arr,
+                             w_arr.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                             u0.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(T), lo, hi,
+                             out.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), int(nthreads))
+    if rc != 0:
+        raise ValueError("oracle_run_cone failed (%d)" % rc)
+    return out
+
+
+def run_window(dims, r: int, offs, w, T: int, lo, hi, u0_block_fn, nthreads: int = 0, cone: bool = True):
     """Exact oracle values on the interior box [lo, hi) after T FIXED steps,
     computed on the dependency-cone window only.  ``u0_block_fn(wlo, whi)``
     returns u0 on the padded-frame window.  Returns an array of shape hi-lo."""
     wlo, whi = window_for(dims, r, T, lo, hi)
     block = u0_block_fn(wlo, whi)
-    wdims = [whi[a] - wlo[a] - 2 * r for a in range(len(dims))]
-    res = run(wdims, r, offs, w, block, T, FIXED, nthreads)
-    sl = tuple(slice(int(lo[a]) + r - wlo[a], int(hi[a]) + r - wlo[a]) for a in range(len(dims)))
+    nd = len(dims)
+    wdims = [whi[a] - wlo[a] - 2 * r for a in range(nd)]
+    blo = [int(lo[a]) + r - wlo[a] - r for a in range(nd)]     # box in window-interior coords
+    bhi = [int(hi[a]) + r - wlo[a] - r for a in range(nd)]
+    if cone:
+        res = run_cone(wdims, r, offs, w, block, T, blo, bhi, nthreads)
+    else:
+        res = run(wdims, r, offs, w, block, T, FIXED, nthreads)
+    sl = tuple(slice(int(lo[a]) + r - wlo[a], int(hi[a]) + r - wlo[a]) for a in range(nd))
     return res[sl]

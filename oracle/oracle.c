@@ -124,6 +124,72 @@ int oracle_run(int nd, const int64_t *dims, int r, int ntaps, const int *offsets
     return 0;
 }
 
+/*
+ * oracle_run_cone: the same T FIXED steps, but step t (1-based) only updates
+ * the interior points within (T - t) * r of the box [blo, bhi) (interior
+ * coordinates).  Those are exactly the points the box's values after T steps
+ * depend on, and each of them is computed with the same arithmetic as in
+ * oracle_run, so the box's values are bit-identical to a full run.  Used on
+ * dependency-cone windows of the full-size configurations.
+ */
+int oracle_run_cone(int nd, const int64_t *dims, int r, int ntaps, const int *offsets,
+                    const double *w, const double *u0, int64_t T, const int64_t *blo,
+                    const int64_t *bhi, double *out, int nthreads) {
+    if (nd < 1 || nd > 3 || r < 1 || ntaps < 1 || T < 0) return -1;
+    int64_t P[3] = {1, 1, 1}, N[3] = {1, 1, 1}, lo3[3] = {0, 0, 0}, hi3[3] = {1, 1, 1};
+    int off = 3 - nd;
+    for (int a = 0; a < nd; ++a) {
+        if (dims[a] < 1) return -1;
+        P[off + a] = dims[a] + 2 * r;
+        N[off + a] = dims[a];
+        lo3[off + a] = blo[a];
+        hi3[off + a] = bhi[a];
+    }
+    int R3[3] = {0, 0, 0};
+    for (int a = 0; a < nd; ++a) R3[off + a] = r;
+    int64_t total = P[0] * P[1] * P[2];
+    int64_t *lin = (int64_t *)malloc(sizeof(int64_t) * ntaps);
+    if (!lin) return -2;
+    for (int j = 0; j < ntaps; ++j) {
+        int64_t o3[3] = {0, 0, 0};
+        for (int a = 0; a < nd; ++a) o3[off + a] = offsets[j * nd + a];
+        lin[j] = (o3[0] * P[1] + o3[1]) * P[2] + o3[2];
+    }
+    double *A = (double *)malloc(sizeof(double) * total);
+    double *B = (double *)malloc(sizeof(double) * total);
+    if (!A || !B) { free(lin); free(A); free(B); return -2; }
+    memcpy(A, u0, sizeof(double) * total);
+    memcpy(B, u0, sizeof(double) * total);
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    for (int64_t t = 1; t <= T; ++t) {
+        int64_t a0[3], a1[3];
+        for (int a = 0; a < 3; ++a) {
+            int64_t e = (a >= off) ? (T - t) * r : 0;
+            a0[a] = lo3[a] - e < 0 ? 0 : lo3[a] - e;
+            a1[a] = hi3[a] + e > N[a] ? N[a] : hi3[a] + e;
+        }
+#ifdef _OPENMP
+#pragma omp parallel for schedule(static)
+#endif
+        for (int64_t z = a0[0]; z < a1[0]; ++z)
+            for (int64_t y = a0[1]; y < a1[1]; ++y)
+                for (int64_t x = a0[2]; x < a1[2]; ++x) {
+                    int64_t p = ((z + R3[0]) * P[1] + (y + R3[1])) * P[2] + (x + R3[2]);
+                    double acc = 0.0;
+                    for (int j = 0; j < ntaps; ++j) acc = acc + w[j] * A[p + lin[j]];
+                    B[p] = acc;
+                }
+        double *tmp = A; A = B; B = tmp;
+    }
+    memcpy(out, A, sizeof(double) * total);
+    free(A); free(B); free(lin);
+    return 0;
+}
+
 /* Thread count the OpenMP runtime would use (for the bench's "cores"). */
 int oracle_max_threads(void) {
 #ifdef _OPENMP

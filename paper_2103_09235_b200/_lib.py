@@ -10,7 +10,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libstencil_b200.so")
+LIB_PATH = os.environ.get("STENCIL_B200_LIB") or os.path.join(HERE, "libstencil_b200.so")
 _lock = threading.Lock()
 _lib = None
 

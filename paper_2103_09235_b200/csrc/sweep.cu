@@ -873,10 +873,25 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
 // Tile configurations:
 //  2D: one row of NTX threads x VX (= 16 B) columns; PB rows per TMA slot.
 //  3D: NTX x NTY threads, each 2 x VY outputs, one plane per TMA slot.
+#ifndef SB_2D_NTX
+#define SB_2D_NTX 256
+#endif
+#ifndef SB_2D_PB
+#define SB_2D_PB 4
+#endif
+#ifndef SB_2D_NSLOT
+#define SB_2D_NSLOT 6
+#endif
+#ifndef SB_3D_NTY
+#define SB_3D_NTY 8
+#endif
+#ifndef SB_3D_NSLOT
+#define SB_3D_NSLOT 4
+#endif
 template <typename T, int SHAPE, int Q, int S>
-using Cfg2 = Cfg<T, 2, SHAPE, 1, Q, S, 128, 1, 1, 4, 4>;
+using Cfg2 = Cfg<T, 2, SHAPE, 1, Q, S, SB_2D_NTX, 1, 1, SB_2D_PB, SB_2D_NSLOT>;
 template <typename T, int SHAPE, int Q, int S>
-using Cfg3 = Cfg<T, 3, SHAPE, 1, Q, S, 32, 8, 2, 1, 4>;
+using Cfg3 = Cfg<T, 3, SHAPE, 1, Q, S, 32, SB_3D_NTY, 2, 1, SB_3D_NSLOT>;
 
 using LaunchFn = int (*)(Plan*, const SweepCall&);
 

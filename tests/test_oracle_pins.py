@@ -268,10 +268,11 @@ def test_window_is_bit_identical(nd, shape, dims, T):
     full = oracle.run(dims, r, offs, w, u0, T)
     for lo in ([0] * nd, [d // 2 for d in dims], [d - 3 for d in dims]):
         hi = [min(l + 3, d) for l, d in zip(lo, dims)]
-        got = oracle.run_window(dims, r, offs, w, T, lo, hi,
-                                lambda a, b: synth.u0_block(dims, r, a, b, 2))
         sl = tuple(slice(l + r, h + r) for l, h in zip(lo, hi))
-        assert np.array_equal(got, full[sl])
+        for cone in (False, True):
+            got = oracle.run_window(dims, r, offs, w, T, lo, hi,
+                                    lambda a, b: synth.u0_block(dims, r, a, b, 2), cone=cone)
+            assert np.array_equal(got, full[sl])
 
 
 def test_generator_counter_form_is_sequential_splitmix64():
