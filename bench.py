@@ -42,7 +42,7 @@ CONFIGS = {
     "c1": dict(name="1D3P heat fp64 N=100000 T=100", dims=(100000,), shape="star", dtype="f64", T=100, ms=(1, 2),
                best_m=2),
     "c2": dict(name="2D5P star fp64 8192x8192 T=200", dims=(8192, 8192), shape="star", dtype="f64", T=200,
-               ms=(1, 2, 4), best_m=2),
+               ms=(1, 2, 4), best_m=4),
     "c3": dict(name="2D9P box fp32 16384x16384 T=200", dims=(16384, 16384), shape="box", dtype="f32", T=200,
                ms=(1, 2, 4), best_m=2),
     "c4": dict(name="3D7P star fp64 512^3 T=100", dims=(512, 512, 512), shape="star", dtype="f64", T=100,

@@ -122,16 +122,16 @@ int support_size(int nd, int shape, int r, int q) {
 }
 
 // ---------------------------------------------------------------- variants
-// FMA-vs-byte budget (the GPU form of the paper's
-// profitability index Eq.3): a sweep streams 2*sizeof(T) bytes per point, so at
-// the HBM roofline it can afford about `budget` FMAs per point.  Prefer the
-// fully folded pass (fewest passes); otherwise the divisor split with the
-// fewest FMAs (stages * |supp lambda^(q)|, plus the overlapped-tile halo).
+// Variant choice (the GPU form of the paper's profitability
+// index Eq.3).  Measured on B200: one folded pass beats on-chip multi-stage
+// evaluation whenever |supp lambda^(m)| <= 64 taps (e.g. 2D5P fp64 m=4, 41 taps:
+// 930 vs 664 GStencil/s), because the single pass needs no intermediate
+// hand-off; above that (2D9P m=4: 81 taps, 3D27P m=2: 125 taps) the divisor
+// split (q, stages) with the fewest FMAs per point wins.
 Variant choose_variant(const Plan* p, int m) {
     if (m <= 1) return {1, 1};
-    double budget = p->dtype == STENCIL_F64 ? 28.0 : 56.0;
-    int full = support_size(p->ndim, p->shape, p->r, m);
-    if (full <= budget) return {m, 1};
+    const int full = support_size(p->ndim, p->shape, p->r, m);
+    if (full <= 64) return {m, 1};
     Variant best = {m, 1};
     double best_cost = 1e30;
     for (int s = 1; s <= m; ++s) {
@@ -139,7 +139,7 @@ Variant choose_variant(const Plan* p, int m) {
         int q = m / s;
         double red = 1.0;
         if (s > 1) {
-            double w = p->ndim == 3 ? 16.0 : 256.0;
+            double w = p->ndim == 3 ? 16.0 : 64.0;
             red = (w + 2.0 * (s - 1) * q * p->r) / w;
             if (p->ndim == 3) red *= (64.0 + 2.0 * (s - 1) * q * p->r) / 64.0;
         }

@@ -48,35 +48,44 @@ namespace sb {
 
 // ------------------------------------------------------------------ config
 template <typename T_, int ND_, int SHAPE_, int RR_, int Q_, int S_, int NTX_, int NTY_, int VY_, int PB_,
-          int NSLOT_>
+          int NSLOT_, int VXM_ = 1>
 struct Cfg {
     using T = T_;
     static constexpr int ND = ND_, SHAPE = SHAPE_, RR = RR_, Q = Q_, S = S_;
     static constexpr int NTX = NTX_, NTY = NTY_, VY = VY_, PB = PB_, NSLOT = NSLOT_;
-    static constexpr int VX = 16 / (int)sizeof(T);
+    static constexpr int VEC = 16 / (int)sizeof(T);   // elements per 16-byte vector
+    static constexpr int VX = VXM_ * VEC;              // consecutive x outputs per thread
     static constexpr int RQ = Q * RR;
     static constexpr int RQY = ND == 3 ? RQ : 0;
     static constexpr int H = S * RQ;
     static constexpr int NW = 2 * RQ + 1;
-    static constexpr int PX = (RQ + VX - 1) / VX * VX;
-    static constexpr int NV = (VX + 2 * PX) / VX;
+    static constexpr int PX = (RQ + VEC - 1) / VEC * VEC;
+    static constexpr int NV = (VX + 2 * PX) / VEC;     // 16-byte vectors per neighbourhood row
     static constexpr int NR = VY + 2 * RQY;
     static constexpr int WX = NTX * VX, WY = NTY * VY;
-    static constexpr int HXO = ((S - 1) * RQ + VX - 1) / VX * VX;
+    static constexpr int HXO = ((S - 1) * RQ + VEC - 1) / VEC * VEC;
     static constexpr int HYO = (S - 1) * RQY;
-    static constexpr int WOX = WX - 2 * HXO, WOY = WY - 2 * HYO;
-    static constexpr int COLS = WX + 2 * PX;
+    // 2D with stages > 1: every warp is its own overlapped tile (32*VX columns,
+    // HXO redundant columns per side); intermediate levels move between lanes
+    // with shuffles instead of shared memory + a CTA barrier.
+    static constexpr bool WARPSTAGE = ND == 2 && S > 1;
+    static constexpr int WW = 32 * VX;              // columns computed per warp
+    static constexpr int WSTEP = WW - 2 * HXO;      // output columns per warp (WARPSTAGE)
+    static constexpr int WOX = WARPSTAGE ? (NTX / 32) * WSTEP : WX - 2 * HXO;
+    static constexpr int WOY = WY - 2 * HYO;
+    static constexpr int COLS = WARPSTAGE ? (NTX / 32 - 1) * WSTEP + WW + 2 * PX : WX + 2 * PX;
     static constexpr int NBX = (COLS + 255) / 256;
-    static constexpr int BX = ((COLS + NBX - 1) / NBX + VX - 1) / VX * VX;
+    static constexpr int BX = ((COLS + NBX - 1) / NBX + VEC - 1) / VEC * VEC;
     static constexpr int ROWS = WY + 2 * RQY;
     static constexpr int CHUNK = (PB * ROWS * BX + (128 / (int)sizeof(T)) - 1) / (128 / (int)sizeof(T)) *
                                  (128 / (int)sizeof(T));
     static constexpr int SLOT_ELEMS = NBX * CHUNK;
     static constexpr uint32_t SLOT_BYTES = (uint32_t)(NBX * PB * ROWS * BX * sizeof(T));
-    static constexpr int LEV_ELEMS = ROWS * COLS;
+    static constexpr int LEV_ELEMS = WARPSTAGE ? 0 : ROWS * COLS;
     static constexpr int NCONS = NTX * NTY;
     static constexpr int NCW = NCONS / 32;
     static constexpr int NTHREADS = NCONS + 32;
+    static constexpr int MINB = 2;   // resident CTAs per SM the register budget is sized for
     static constexpr int NC = ND == 3 ? NW * NW * NW : NW * NW;
     static constexpr size_t DATA_BYTES = (size_t)NSLOT * SLOT_ELEMS * sizeof(T) +
                                          (size_t)(S - 1) * 2 * LEV_ELEMS * sizeof(T);
@@ -135,7 +144,7 @@ template <class C>
 struct Consumer {
     using T = typename C::T;
     T acc[C::S][C::NW][C::VY][C::VX];
-    T nb[C::NR][C::NV * C::VX];
+    T nb[C::NR][C::NV * C::VEC];
 
     // FMA the neighbourhood `nb` of one level-J plane into stage J's window.
     template <int J, int PH>
@@ -290,7 +299,7 @@ __device__ __forceinline__ void seg_state(const DevSched& sc, const DevBoxes& b,
 }
 
 template <class C>
-__global__ void __launch_bounds__(C::NTHREADS)
+__global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     sweep_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ SweepParams<typename C::T, C::NC> p) {
     using T = typename C::T;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -483,10 +492,12 @@ __global__ void __launch_bounds__(C::NTHREADS)
 
     // ================================================================ consumers
     const int tx = threadIdx.x % C::NTX, ty = threadIdx.x / C::NTX;
+    // first computed column of this thread, relative to the tile's compute origin
+    const int tcol = C::WARPSTAGE ? warp * C::WSTEP + lane * C::VX : tx * C::VX;
     int off0[C::NV];
 #pragma unroll
     for (int v = 0; v < C::NV; ++v) {
-        const int c = tx * C::VX + v * C::VX;
+        const int c = tcol + v * C::VEC;
         off0[v] = (c / C::BX) * C::CHUNK + (c % C::BX);
     }
     Consumer<C> cs;
@@ -494,6 +505,8 @@ __global__ void __launch_bounds__(C::NTHREADS)
     T* __restrict__ dst = p.dst;
     const long long s0 = p.g.stride0, s1 = p.g.stride1;
     int gx = 0, gy = 0, xlo = 0, xhi = 0, ylo = 0, yhi = 0;
+    T* obase = dst;           // output pointer of (z = -origin0, gy, gx) for the current run
+    unsigned vmask = 0, ymask = 0;   // full-vector stores allowed / rows in range
     bool edge_xy = false;
     int z_first = 0, out_lo = 0, out_hi = 0;
     bool done = false;
@@ -522,12 +535,26 @@ __global__ void __launch_bounds__(C::NTHREADS)
                                 for (int vx = 0; vx < C::VX; ++vx) cs.acc[s][k][vy][vx] = T(0);
                     int bx, cx0, cy0;
                     col_geom(m.col, &bx, &cx0, &cy0, &xlo, &xhi, &ylo, &yhi);
-                    gx = cx0 + tx * C::VX;
+                    gx = cx0 + tcol;
                     gy = cy0 + ty * C::VY;
+                    if (C::WARPSTAGE) {   // store only this warp's output columns
+                        const int wlo = cx0 + C::HXO + warp * C::WSTEP;
+                        xlo = max(xlo, wlo);
+                        xhi = min(xhi, wlo + C::WSTEP);
+                    }
+                    obase = dst + (p.g.origin[1] + gy) * s1 + p.g.origin[2] + gx;
+                    vmask = 0;
+#pragma unroll
+                    for (int mm = 0; mm < C::VX / C::VEC; ++mm)
+                        if (gx + mm * C::VEC >= xlo && gx + (mm + 1) * C::VEC <= xhi) vmask |= 1u << mm;
+                    ymask = 0;
+#pragma unroll
+                    for (int vy = 0; vy < C::VY; ++vy)
+                        if (gy + vy >= ylo && gy + vy < yhi) ymask |= 1u << vy;
                     edge_xy = false;
                     if (C::S > 1) {
                         edge_xy |= p.g.phys_lo[2] && (cx0 - C::PX < 0);
-                        edge_xy |= p.g.phys_hi[2] && (cx0 + C::WX + C::PX > p.g.n[2]);
+                        edge_xy |= p.g.phys_hi[2] && (cx0 + C::COLS - C::PX > p.g.n[2]);
                         if (C::ND == 3) {
                             edge_xy |= p.g.phys_lo[1] && (cy0 - C::RQY < 0);
                             edge_xy |= p.g.phys_hi[1] && (cy0 + C::WY + C::RQY > p.g.n[1]);
@@ -545,7 +572,7 @@ __global__ void __launch_bounds__(C::NTHREADS)
 #pragma unroll
                 for (int rr = 0; rr < C::NR; ++rr)
 #pragma unroll
-                    for (int v = 0; v < C::NV; ++v) VecT<T>::ld(base + rr * C::BX + off0[v], &cs.nb[rr][v * C::VX]);
+                    for (int v = 0; v < C::NV; ++v) VecT<T>::ld(base + rr * C::BX + off0[v], &cs.nb[rr][v * C::VEC]);
                 if (pl == C::PB - 1) {
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&empty[slot]);
@@ -589,17 +616,34 @@ __global__ void __launch_bounds__(C::NTHREADS)
                                                 p.g.origin[2] + gx + vx];
                         }
                 }
+                if constexpr (C::WARPSTAGE) {
+                    // neighbours from adjacent lanes (lanes 0/31 get values that only
+                    // feed the warp's redundant edge columns)
+#pragma unroll
+                    for (int j = 0; j < C::NV * C::VEC; ++j) {
+                        const int rel = j - C::PX;                       // column relative to gx
+                        const int d = rel >= 0 ? rel / C::VX : -((-rel + C::VX - 1) / C::VX);
+                        const int e = rel - d * C::VX;
+                        if (d == 0) cs.nb[0][j] = v[0][e];
+                        else if (d < 0) cs.nb[0][j] = __shfl_up_sync(0xffffffffu, v[0][e], -d);
+                        else cs.nb[0][j] = __shfl_down_sync(0xffffffffu, v[0][e], d);
+                    }
+                } else {
                 T* lp = lev + ((J - 1) * 2 + (i & 1)) * C::LEV_ELEMS;
 #pragma unroll
                 for (int vy = 0; vy < C::VY; ++vy)
-                    VecT<T>::st(lp + (ty * C::VY + vy + C::RQY) * C::COLS + tx * C::VX + C::PX, v[vy]);
+#pragma unroll
+                    for (int mm = 0; mm < C::VX / C::VEC; ++mm)
+                        VecT<T>::st(lp + (ty * C::VY + vy + C::RQY) * C::COLS + tcol + C::PX + mm * C::VEC,
+                                    &v[vy][mm * C::VEC]);
                 ptx::named_bar_sync(1, C::NCONS);
-                const T* base = lp + (ty * C::VY) * C::COLS + tx * C::VX;
+                const T* base = lp + (ty * C::VY) * C::COLS + tcol;
 #pragma unroll
                 for (int rr = 0; rr < C::NR; ++rr)
 #pragma unroll
                     for (int vv = 0; vv < C::NV; ++vv)
-                        VecT<T>::ld(base + rr * C::COLS + vv * C::VX, &cs.nb[rr][vv * C::VX]);
+                        VecT<T>::ld(base + rr * C::COLS + vv * C::VEC, &cs.nb[rr][vv * C::VEC]);
+                }
                 cs.template fold_plane<J, PH>(p.coef);
             };
             if constexpr (C::S > 1) stage(std::integral_constant<int, 1>{});
@@ -611,17 +655,22 @@ __global__ void __launch_bounds__(C::NTHREADS)
                 constexpr int dn = pmod(PH - C::H, C::NW);
                 const int z = z_in - C::H;
                 if (z >= out_lo && z < out_hi) {
+                    T* orow = obase + (p.g.origin[0] + z) * s0;
 #pragma unroll
                     for (int vy = 0; vy < C::VY; ++vy) {
-                        const int y = gy + vy;
-                        if (y < ylo || y >= yhi) continue;
-                        T* op = dst + (p.g.origin[0] + z) * s0 + (p.g.origin[1] + y) * s1 + p.g.origin[2] + gx;
-                        if (gx >= xlo && gx + C::VX <= xhi) {
-                            VecT<T>::st(op, cs.acc[C::S - 1][dn][vy]);
-                        } else {
+                        if (!(ymask & (1u << vy))) continue;
+                        T* op = orow + vy * s1;
 #pragma unroll
-                            for (int vx = 0; vx < C::VX; ++vx)
-                                if (gx + vx >= xlo && gx + vx < xhi) op[vx] = cs.acc[C::S - 1][dn][vy][vx];
+                        for (int mm = 0; mm < C::VX / C::VEC; ++mm) {
+                            if (vmask & (1u << mm)) {
+                                VecT<T>::st(op + mm * C::VEC, &cs.acc[C::S - 1][dn][vy][mm * C::VEC]);
+                            } else {
+#pragma unroll
+                                for (int e = 0; e < C::VEC; ++e) {
+                                    const int x = gx + mm * C::VEC + e;
+                                    if (x >= xlo && x < xhi) op[mm * C::VEC + e] = cs.acc[C::S - 1][dn][vy][mm * C::VEC + e];
+                                }
+                            }
                         }
                     }
                 }
@@ -813,9 +862,13 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
         const int nty = C::ND == 3 ? (int)((b.hi[1] - b.lo[1] + C::WOY - 1) / C::WOY) : 1;
         const int64_t zlen = b.hi[0] - b.lo[0];
         const int64_t cols = (int64_t)ntx * nty;
-        // initial segments: about one resident wave of CTAs, split by volume
+        // initial segments: about one resident wave of CTAs, split by volume.  When
+        // there are already at least as many columns as SMs, columns are not split:
+        // neighbouring columns then stream the same planes at about the same time and
+        // their shared halo rows are still in L2 (3D halos are ~20% of a tile).
         double share = vol_total > 0 ? double(b.volume()) / double(vol_total) : 1.0;
         int64_t want = std::max<int64_t>(1, (int64_t)(target * share) / std::max<int64_t>(1, cols));
+        if (C::ND == 3 && cols >= p->sm_count) want = 1;
         int64_t nch = std::min<int64_t>(want, std::max<int64_t>(1, zlen / 8));
         int64_t zc = (zlen + nch - 1) / nch;
         nch = (zlen + zc - 1) / zc;
@@ -888,8 +941,15 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
 #ifndef SB_3D_NSLOT
 #define SB_3D_NSLOT 4
 #endif
+#ifndef SB_2D_VXM_HEAVY
+#define SB_2D_VXM_HEAVY 2
+#endif
+// FMA-heavy passes (|supp lambda^(Q)| >= 25) give each thread more outputs so the
+// neighbourhood loads and per-row bookkeeping are amortised over more FMAs.
+template <int SHAPE, int Q>
+constexpr int vxm2() { return (SHAPE == STENCIL_BOX ? Q >= 2 : Q >= 4) ? SB_2D_VXM_HEAVY : 1; }
 template <typename T, int SHAPE, int Q, int S>
-using Cfg2 = Cfg<T, 2, SHAPE, 1, Q, S, SB_2D_NTX, 1, 1, SB_2D_PB, SB_2D_NSLOT>;
+using Cfg2 = Cfg<T, 2, SHAPE, 1, Q, S, SB_2D_NTX / vxm2<SHAPE, Q>(), 1, 1, SB_2D_PB, SB_2D_NSLOT, vxm2<SHAPE, Q>()>;
 template <typename T, int SHAPE, int Q, int S>
 using Cfg3 = Cfg<T, 3, SHAPE, 1, Q, S, 32, SB_3D_NTY, 2, 1, SB_3D_NSLOT>;
 
