@@ -4,6 +4,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <cstdlib>
+#include <utility>
 
 #include "internal.hpp"
 #include "sweep_params.cuh"
@@ -16,70 +18,154 @@ int cuda_error(int e, const char* what) {
 
 // ============================================================== K-G4 1D
 // 1D: the whole grid (0.8 MB for the 1D3P config) is far below L2 and one sweep
-// is shorter than a launch, so TB time steps run inside one launch: each CTA
-// owns B outputs, loads them plus a TB*r halo into shared memory and applies
-// TB/m folded steps (lambda^(m)) then TB mod m single steps on a shrinking
-// region (overlapped tiles, no inter-CTA synchronisation).  CTAs whose region
-// comes within (m-1)*r of a FIXED face apply single steps throughout (exact
-// band, R2); ring cells keep u0.
-constexpr int K1_THREADS = 256;
-constexpr int K1_MAXC = 2 * STENCIL_MAX_FOLD * 4 + 1;
+// is shorter than a launch, so TB time steps run inside one launch.  Every
+// WARP is its own overlapped tile (no shared memory, no barriers): lane l
+// holds the V consecutive cells [ilo + l*V, ilo + l*V + V) of the warp's
+// window in registers, the 2*R neighbours it needs from lanes l-1 / l+1 come
+// through warp shuffles, and the window shrinks by R per step (its 32*V - 2H
+// middle cells, H = TB*r, are exact after TB steps and are the ones stored).
+// The warp applies TB/m folded steps (lambda^(m), radius RF = m*r, Eq.2) and
+// then TB mod m single steps (radius RS = r).  Warps whose window comes within
+// (m-1)*r of a FIXED face apply single steps throughout, with the ring cells
+// frozen at u0 (exact band, R2).  Thread 0..31 of block 0 also copy
+// the non-interior cells (ring + pads) src -> dst, so a launch is the whole
+// sweep (no separate ring-copy launch).
+constexpr int K1_THREADS = 128;
+constexpr int K1_MAXC = 2 * 32 + 1;
 
 template <typename T>
 struct Params1D {
     const T* src;
     T* dst;
     long long origin, ext;
-    int n, r, m, TB, B, force_step;
-    int nlam, nw;
+    int n, r, m, TB, B, nwarps, force_step;
     T lam[K1_MAXC];   // lambda^(m), index o + m r
     T w[9];           // original taps, index o + r
 };
 
-template <typename T>
-__global__ void __launch_bounds__(K1_THREADS) onchip1d_kernel(const __grid_constant__ Params1D<T> p) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    const int hal = p.TB * p.r;
-    const int x0 = blockIdx.x * p.B;
-    const int x1 = min(x0 + p.B, p.n);
-    const int ilo = x0 - hal;
-    const int len = (x1 - x0) + 2 * hal;
-    T* a = reinterpret_cast<T*>(smem_raw);
-    T* b = a + len;
-    for (int e = threadIdx.x; e < len; e += blockDim.x) {
-        long long g = p.origin + ilo + e;
-        a[e] = (g >= 0 && g < p.ext) ? p.src[g] : T(0);
+// One step of radius R on the lane's V cells a -> b (neighbours by shuffle).
+// FROZEN: cells whose bit is set in `frozen` keep their value (ring cells).
+template <typename T, int V, int R, bool FROZEN>
+__device__ __forceinline__ void step1d(const T (&a)[V], T (&b)[V], const T (&c)[2 * R + 1], unsigned frozen) {
+    static_assert(R <= V, "neighbours must come from the adjacent lane");
+    T lft[R], rgt[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+        lft[j] = __shfl_up_sync(0xffffffffu, a[V - R + j], 1);   // cell l*V - R + j
+        rgt[j] = __shfl_down_sync(0xffffffffu, a[j], 1);         // cell l*V + V + j
     }
-    __syncthreads();
-    const int band = (p.m - 1) * p.r;
-    const bool stepwise = p.force_step || (ilo < band) || (x1 + hal > p.n - band);
-    const int nfold = stepwise ? 0 : p.TB / p.m;
-    const int nsingle = stepwise ? p.TB : p.TB % p.m;
-    int shrink = 0;
-    for (int s = 0; s < nfold + nsingle; ++s) {
-        const bool fold = s < nfold;
-        const int R = fold ? p.m * p.r : p.r;
-        shrink += R;
-        for (int e = shrink + threadIdx.x; e < len - shrink; e += blockDim.x) {
-            const int x = ilo + e;
-            T acc;
-            if (x < 0 || x >= p.n) {
-                acc = a[e];   // frozen ring (or unused cells beyond it)
-            } else if (fold) {
-                acc = T(0);
-                for (int o = -R; o <= R; ++o) acc = fma(p.lam[o + R], a[e + o], acc);
-            } else {
-                acc = T(0);
-                for (int o = -R; o <= R; ++o) acc = fma(p.w[o + R], a[e + o], acc);
-            }
-            b[e] = acc;
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        T acc = T(0);
+#pragma unroll
+        for (int o = -R; o <= R; ++o) {
+            const int i = v + o;
+            const T x = i < 0 ? lft[i + R] : (i >= V ? rgt[i - V] : a[i]);
+            acc = fma(c[o + R], x, acc);
         }
-        __syncthreads();
-        T* t = a;
-        a = b;
-        b = t;
+        b[v] = (FROZEN && ((frozen >> v) & 1u)) ? a[v] : acc;
     }
-    for (int e = threadIdx.x; e < x1 - x0; e += blockDim.x) p.dst[p.origin + x0 + e] = a[hal + e];
+}
+
+template <typename T, int V, int R, bool FROZEN>
+__device__ __forceinline__ void steps1d(T (&a)[V], T (&b)[V], const T* __restrict__ cp, int n, unsigned frozen) {
+    T c[2 * R + 1];   // coefficients in registers for the whole time loop
+#pragma unroll
+    for (int j = 0; j <= 2 * R; ++j) c[j] = cp[j];
+#pragma unroll 1
+    for (int s = 0; s + 1 < n; s += 2) {
+        step1d<T, V, R, FROZEN>(a, b, c, frozen);
+        step1d<T, V, R, FROZEN>(b, a, c, frozen);
+    }
+    if (n & 1) {
+        step1d<T, V, R, FROZEN>(a, b, c, frozen);
+#pragma unroll
+        for (int v = 0; v < V; ++v) a[v] = b[v];
+    }
+}
+
+template <typename T, int V, int RF, int RS>
+__global__ void __launch_bounds__(K1_THREADS) onchip1d_kernel(const __grid_constant__ Params1D<T> p) {
+    if (blockIdx.x == 0 && threadIdx.x < 32) {   // ring + pads (never written by the steps)
+        for (long long g = threadIdx.x; g < p.origin; g += 32) p.dst[g] = p.src[g];
+        for (long long g = p.origin + p.n + threadIdx.x; g < p.ext; g += 32) p.dst[g] = p.src[g];
+    }
+    const int gw = blockIdx.x * (K1_THREADS / 32) + (threadIdx.x >> 5);
+    if (gw >= p.nwarps) return;   // whole warp
+    const int lane = threadIdx.x & 31;
+    const int H = p.TB * p.r;
+    const int x0 = gw * p.B;                 // first output of this warp
+    const int x1 = min(x0 + p.B, p.n);
+    const int ilo = x0 - H;                  // first cell of the window
+    const int c0 = ilo + lane * V;           // first cell of this lane
+    T a[V], b[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const long long g = p.origin + c0 + v;
+        a[v] = (g >= 0 && g < p.ext) ? p.src[g] : T(0);
+    }
+    const int band = (p.m - 1) * p.r;
+    const bool stepwise = p.force_step || ilo < band || x1 + H > p.n - band;
+    if (!stepwise) {
+        steps1d<T, V, RF, false>(a, b, p.lam, p.TB / p.m, 0u);
+        steps1d<T, V, RS, false>(a, b, p.w, p.TB % p.m, 0u);
+    } else {
+        unsigned frozen = 0;   // cells outside the interior keep u0 (ring; beyond it: never read by valid cells)
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (c0 + v < 0 || c0 + v >= p.n) frozen |= 1u << v;
+        steps1d<T, V, RS, true>(a, b, p.w, p.TB, frozen);
+    }
+#pragma unroll
+    for (int v = 0; v < V; ++v) {
+        const int x = c0 + v;
+        if (x >= x0 && x < x1) p.dst[p.origin + x] = a[v];
+    }
+}
+
+template <typename T>
+using K1Fn = void (*)(Params1D<T>);
+
+// dispatch table over (V in {8, 16, 32}, RS = r in 1..4, m in 1..8); V >= m*r.
+template <typename T, int V, int RS, int M>
+constexpr K1Fn<T> k1_entry() {
+    constexpr int RF = RS * M;
+    if constexpr (RF <= V) return onchip1d_kernel<T, V, RF, RS>;
+    else return nullptr;
+}
+template <typename T, int V, int RS, int... Ms>
+constexpr void k1_row(K1Fn<T>* row, std::integer_sequence<int, Ms...>) {
+    ((row[Ms] = k1_entry<T, V, RS, Ms + 1>()), ...);
+}
+template <typename T, int V>
+static K1Fn<T> k1_pick_v(int r, int m) {
+    static K1Fn<T> tab[4][8] = {};
+    static bool init = false;
+    if (!init) {
+        k1_row<T, V, 1>(tab[0], std::make_integer_sequence<int, 8>{});
+        k1_row<T, V, 2>(tab[1], std::make_integer_sequence<int, 8>{});
+        k1_row<T, V, 3>(tab[2], std::make_integer_sequence<int, 8>{});
+        k1_row<T, V, 4>(tab[3], std::make_integer_sequence<int, 8>{});
+        init = true;
+    }
+    if (r < 1 || r > 4 || m < 1 || m > 8) return nullptr;
+    return tab[r - 1][m - 1];
+}
+template <typename T>
+static K1Fn<T> k1_pick(int V, int r, int m) {
+    return V == 8 ? k1_pick_v<T, 8>(r, m) : V == 16 ? k1_pick_v<T, 16>(r, m) : k1_pick_v<T, 32>(r, m);
+}
+
+// Cells per lane: the smallest of {8, 16, 32} holding the fold radius; the
+// env var STENCIL_1D_V overrides it (tuning).
+int onchip1d_cells_per_lane(int r, int m) {
+    static int forced = [] {
+        const char* e = getenv("STENCIL_1D_V");
+        return e ? atoi(e) : 0;
+    }();
+    int v = r * m <= 8 ? 8 : r * m <= 16 ? 16 : 32;
+    if ((forced == 8 || forced == 16 || forced == 32) && forced >= r * m) v = forced;
+    return v;
 }
 
 template <typename T>
@@ -98,23 +184,17 @@ static int launch_1d_t(Plan* p, const void* src, void* dst, const Layout3* L, in
     prm.force_step = force_step ? 1 : 0;
     const std::vector<double>& lam = folded(p, m);
     if ((int)lam.size() > K1_MAXC || (int)p->w.size() > 9) return set_error(STENCIL_EUNSUPPORTED, "1D fold too wide");
-    prm.nlam = (int)lam.size();
     for (size_t i = 0; i < lam.size(); ++i) prm.lam[i] = static_cast<T>(lam[i]);
-    prm.nw = (int)p->w.size();
     for (size_t i = 0; i < p->w.size(); ++i) prm.w[i] = static_cast<T>(p->w[i]);
-    // about two CTAs per SM, each B outputs (+ 2*TB*r halo)
-    int nctas = std::max(1, 2 * p->sm_count);
-    int B = (int)std::max<int64_t>(64, (prm.n + nctas - 1) / nctas);
-    prm.B = B;
-    nctas = (prm.n + B - 1) / B;
-    size_t smem = 2 * (size_t)(B + 2 * TB * p->r) * sizeof(T);
-    if (smem > 200 * 1024) return set_error(STENCIL_EUNSUPPORTED, "1D on-chip block too large");
-    static bool attr_set[2] = {false, false};
-    if (!attr_set[sizeof(T) == 8]) {
-        cudaFuncSetAttribute(onchip1d_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr_set[sizeof(T) == 8] = true;
-    }
-    onchip1d_kernel<T><<<nctas, K1_THREADS, smem, (cudaStream_t)stream>>>(prm);
+    const int V = onchip1d_cells_per_lane(p->r, m);
+    K1Fn<T> fn = k1_pick<T>(V, p->r, m);
+    if (!fn) return set_error(STENCIL_EUNSUPPORTED, "1D kernel: r or fold_m out of range");
+    prm.B = 32 * V - 2 * (int)TB * p->r;   // outputs per warp
+    if (prm.B <= 0) return set_error(STENCIL_EINVAL, "1D kernel: too many steps per launch for the warp window");
+    prm.nwarps = (prm.n + prm.B - 1) / prm.B;
+    const int wpb = K1_THREADS / 32;
+    const unsigned blocks = (unsigned)std::max(1, (prm.nwarps + wpb - 1) / wpb);
+    fn<<<blocks, K1_THREADS, 0, (cudaStream_t)stream>>>(prm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "onchip1d_kernel launch");
     return 1;

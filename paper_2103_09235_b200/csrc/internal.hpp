@@ -97,6 +97,7 @@ int launch_sweep(Plan* p, const SweepCall& c);
 // 1D on-chip multi-step kernel (K-G4): T steps (fold m) in one launch.
 int launch_1d(Plan* p, const void* src, void* dst, const Layout3* L, int64_t T, int m,
               int stages_flag, void* stream);
+int onchip1d_cells_per_lane(int r, int m);   // V of the warp window (32*V cells)
 
 // Copy every non-interior cell (ring, ghosts, pads) src -> dst (K-G5).
 int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void* stream);

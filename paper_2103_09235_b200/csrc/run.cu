@@ -8,6 +8,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -169,20 +170,26 @@ static int check_run_args(Plan* p, const void* in, void* out, int64_t T, int m, 
 // ------------------------------------------------------------------ 1D
 static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t T, int m, int stages, void* ws,
                   void* stream) {
-    const int64_t cap = std::max<int64_t>(m, 128 / m * m);
+    // steps per launch: the warp window (32*V cells) keeps at least half of its
+    // cells as outputs, i.e. a halo H = TB*r <= 8*V; a multiple of m
+    // (STENCIL_1D_HMAX overrides the 8*V halo bound: tuning)
+    const int V = onchip1d_cells_per_lane(p->r, m);
+    static const int64_t hforce = [] {
+        const char* e = getenv("STENCIL_1D_HMAX");
+        return e ? (int64_t)atoll(e) : (int64_t)0;
+    }();
+    const int64_t hmax = std::min<int64_t>(hforce > 0 ? hforce : 8 * V, 16 * V - 1) / p->r;
+    int64_t cap = std::max<int64_t>(m, hmax / m * m);
     int64_t nl = (T + cap - 1) / cap;
+    cap = std::max<int64_t>(m, ((T + nl - 1) / nl + m - 1) / m * m);   // balance the launches
+    nl = (T + cap - 1) / cap;
     if (nl >= 2 && !ws) return set_error(STENCIL_EINVAL, "workspace required");
     bool force_step = (stages == m && m > 1);
-    int rc = launch_ring_copy(p, in, out, &L, stream);
-    if (rc < 0) return rc;
-    int launches = rc;
-    if (nl >= 2) {
-        rc = launch_ring_copy(p, in, ws, &L, stream);
-        if (rc < 0) return rc;
-        launches += rc;
-    }
+    int launches = 0;
+    int rc = 0;
     void* bufs[2] = {out, ws};
     int64_t left = T;
+    const int64_t k = (int64_t)p->w.size();
     for (int64_t j = 1; j <= nl; ++j) {
         int64_t tb = std::min(cap, left);
         left -= tb;
@@ -190,8 +197,8 @@ static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t 
         void* dst = bufs[(nl - j) % 2];
         {
             TimedScope ts(p, stream, 0, 2 * L.esize * L.n[2],
-                          L.n[2] * (force_step ? tb * 3 : (tb / m) * support_size(1, p->shape, p->r, m) +
-                                                              (tb % m) * (int64_t)p->w.size()));
+                          L.n[2] * (force_step ? tb * k : (tb / m) * support_size(1, p->shape, p->r, m) +
+                                                              (tb % m) * k));
             rc = launch_1d(p, src, dst, &L, tb, m, force_step ? 1 : 0, stream);
         }
         if (rc < 0) return rc;

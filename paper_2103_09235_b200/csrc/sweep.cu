@@ -48,7 +48,7 @@ namespace sb {
 
 // ------------------------------------------------------------------ config
 template <typename T_, int ND_, int SHAPE_, int RR_, int Q_, int S_, int NTX_, int NTY_, int VY_, int PB_,
-          int NSLOT_, int VXM_ = 1>
+          int NSLOT_, int VXM_ = 1, int MINB_ = 2, int ROT_ = 0, int PINC_ = 0>
 struct Cfg {
     using T = T_;
     static constexpr int ND = ND_, SHAPE = SHAPE_, RR = RR_, Q = Q_, S = S_;
@@ -85,7 +85,15 @@ struct Cfg {
     static constexpr int NCONS = NTX * NTY;
     static constexpr int NCW = NCONS / 32;
     static constexpr int NTHREADS = NCONS + 32;
-    static constexpr int MINB = 2;   // resident CTAs per SM the register budget is sized for
+    static constexpr int MINB = MINB_;   // resident CTAs per SM the register budget is sized for
+    // ROT = 1: one loop iteration per plane, the window slots renamed by a
+    // register rotation (NW-1 moves per output) instead of unrolling the loop
+    // over the NW window phases (NW x smaller hot loop: instruction-cache fit).
+    static constexpr bool ROT = ROT_ != 0;
+    // PINC = 1: the folded coefficients are pinned in registers for the whole
+    // kernel (otherwise the compiler may re-load them from the constant bank
+    // every plane).
+    static constexpr bool PINC = PINC_ != 0;
     static constexpr int NC = ND == 3 ? NW * NW * NW : NW * NW;
     static constexpr size_t DATA_BYTES = (size_t)NSLOT * SLOT_ELEMS * sizeof(T) +
                                          (size_t)(S - 1) * 2 * LEV_ELEMS * sizeof(T);
@@ -114,6 +122,10 @@ struct VecT;
 template <>
 struct VecT<double> {
     using V = double2;
+    // 16-byte shared-memory load from a 32-bit shared-window address
+    static __device__ __forceinline__ void lds(uint32_t a, double* out) {
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(out[0]), "=d"(out[1]) : "r"(a));
+    }
     static __device__ __forceinline__ void ld(const double* p, double* out) {
         double2 v = *reinterpret_cast<const double2*>(p);
         out[0] = v.x;
@@ -125,6 +137,11 @@ struct VecT<double> {
 };
 template <>
 struct VecT<float> {
+    static __device__ __forceinline__ void lds(uint32_t a, float* out) {
+        asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                     : "=f"(out[0]), "=f"(out[1]), "=f"(out[2]), "=f"(out[3])
+                     : "r"(a));
+    }
     static __device__ __forceinline__ void ld(const float* p, float* out) {
         float4 v = *reinterpret_cast<const float4*>(p);
         out[0] = v.x;
@@ -138,36 +155,61 @@ struct VecT<float> {
 };
 
 __device__ __forceinline__ double fmaT(double a, double b, double c) { return fma(a, b, c); }
+// Opaque copies: the compiler cannot rematerialise (re-load) the result, so
+// loop-invariant coefficients / addresses stay in registers across the plane loop.
+__device__ __forceinline__ double pin(double v) {
+    double r;
+    asm volatile("mov.b64 %0, %1;" : "=d"(r) : "d"(v));
+    return r;
+}
+__device__ __forceinline__ float pin(float v) {
+    float r;
+    asm volatile("mov.b32 %0, %1;" : "=f"(r) : "f"(v));
+    return r;
+}
+__device__ __forceinline__ uint32_t pin(uint32_t v) {
+    uint32_t r;
+    asm volatile("mov.b32 %0, %1;" : "=r"(r) : "r"(v));
+    return r;
+}
 __device__ __forceinline__ float fmaT(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
 template <class C>
 struct Consumer {
     using T = typename C::T;
     T acc[C::S][C::NW][C::VY][C::VX];
-    T nb[C::NR][C::NV * C::VEC];
 
-    // FMA the neighbourhood `nb` of one level-J plane into stage J's window.
-    template <int J, int PH>
-    __device__ __forceinline__ void fold_plane(const T* __restrict__ coef) {
+    // FMA one level-J plane into stage J's window, streaming its neighbourhood
+    // row by row: `ld(rr, row)` fetches row rr (NV 16-byte vectors) of the
+    // thread's (VY + 2*RQY) x (VX + 2*PX) neighbourhood, which is applied to
+    // every pending output row that uses it, so only one row is live.
+    template <int J, int PH, class LD>
+    __device__ __forceinline__ void fold_plane(const T (&coef)[C::NC], LD&& ld) {
         constexpr int RQ = C::RQ, RQY = C::RQY, NW = C::NW;
 #pragma unroll
-        for (int k = 0; k < NW; ++k) {
-            const int oz = RQ - k;
-            const int idx = pmod(PH - J * RQ - RQ + k, NW);
+        for (int rr = 0; rr < C::NR; ++rr) {
+            T row[C::NV * C::VEC];
+            ld(rr, row);
 #pragma unroll
-            for (int oy = -RQY; oy <= RQY; ++oy)
+            for (int k = 0; k < NW; ++k) {
+                const int oz = RQ - k;
+                const int idx = pmod(PH - J * RQ - RQ + k, NW);
 #pragma unroll
-                for (int ox = -RQ; ox <= RQ; ++ox) {
-                    if (!in_support<C::SHAPE, C::RR, C::Q>(oz, oy, ox)) continue;
-                    const int ci = C::ND == 3 ? ((oz + RQ) * (2 * RQY + 1) + (oy + RQY)) * (2 * RQ + 1) + (ox + RQ)
-                                              : (oz + RQ) * (2 * RQ + 1) + (ox + RQ);
-                    const T c = coef[ci];
+                for (int oy = -RQY; oy <= RQY; ++oy) {
+                    const int vy = rr - oy - RQY;
+                    if (vy < 0 || vy >= C::VY) continue;
 #pragma unroll
-                    for (int vy = 0; vy < C::VY; ++vy)
+                    for (int ox = -RQ; ox <= RQ; ++ox) {
+                        if (!in_support<C::SHAPE, C::RR, C::Q>(oz, oy, ox)) continue;
+                        const int ci = C::ND == 3 ? ((oz + RQ) * (2 * RQY + 1) + (oy + RQY)) * (2 * RQ + 1) + (ox + RQ)
+                                                  : (oz + RQ) * (2 * RQ + 1) + (ox + RQ);
+                        const T c = coef[ci];
 #pragma unroll
                         for (int vx = 0; vx < C::VX; ++vx)
-                            acc[J][idx][vy][vx] = fmaT(c, nb[vy + oy + RQY][vx + ox + C::PX], acc[J][idx][vy][vx]);
+                            acc[J][idx][vy][vx] = fmaT(c, row[vx + ox + C::PX], acc[J][idx][vy][vx]);
+                    }
                 }
+            }
         }
     }
 };
@@ -177,9 +219,35 @@ struct Consumer {
 // faces to the r-wide ring: nothing beyond the ring is ever needed), run m
 // single steps of the ORIGINAL taps on the shrinking region, ring cells
 // frozen at u0 (R1/R2), store the block.
-template <typename T>
-__device__ __forceinline__ void band_block(const BandDesc<T>& bd, const DevGeom& g, const T* __restrict__ src,
-                                        T* __restrict__ dst, int blk_id, T* smem, int tid, int nthr) {
+//
+// Work is distributed by rows (fixed axis-0/axis-1 coordinates): a warp takes
+// 32/LX rows at a time, LX = the smallest power of two >= the row length (at
+// most 32), so thin x-face blocks keep the warp busy and there is one integer
+// division per row, not per cell.  The taps are unrolled at compile time in
+// canonical order (R4) with shared-memory offsets o0*S0 + o1*S1 + o2.
+template <class C, class F>
+__device__ __forceinline__ void band_rows(int n0, int n1, int n2, int tid, int nthr, F&& f) {
+    const int warp = tid >> 5, lane = tid & 31, nwarp = nthr >> 5;
+    int lg = 5;
+    while (lg > 0 && (1 << (lg - 1)) >= n2) --lg;
+    const int LX = 1 << lg, RPW = 32 >> lg;
+    const int lx = lane & (LX - 1), lr = lane >> lg;
+    const int rows = n0 * n1;
+    for (int rb = warp * RPW; rb < rows; rb += nwarp * RPW) {
+        const int row = rb + lr;
+        if (row >= rows) continue;
+        const int c1 = row % n1, c0 = row / n1;
+        f(c0, c1, lx, LX);
+    }
+}
+
+template <class C>
+__device__ __forceinline__ void band_block(const BandDesc<typename C::T>& bd, const DevGeom& g,
+                                           const typename C::T* __restrict__ src, typename C::T* __restrict__ dst,
+                                           int blk_id, typename C::T* smem, int tid, int nthr) {
+    using T = typename C::T;
+    constexpr int RR = C::RR;
+    constexpr bool used[3] = {true, C::ND == 3, true};
     int b = 0;
     while (b + 1 < bd.nbox && blk_id >= bd.begin[b + 1]) ++b;
     int t = blk_id - bd.begin[b];
@@ -193,66 +261,78 @@ __device__ __forceinline__ void band_block(const BandDesc<T>& bd, const DevGeom&
     for (int a = 0; a < 3; ++a) {
         olo[a] = bd.lo[b][a] + bi[a] * bd.blk[b][a];
         ohi[a] = min(olo[a] + bd.blk[b][a], bd.hi[b][a]);
-        const int H = bd.used[a] ? bd.m * bd.r : 0;
+        const int H = used[a] ? bd.m * RR : 0;
         int lo = olo[a] - H, hi = ohi[a] + H;
-        clo[a] = bd.used[a] && g.phys_lo[a] && lo < -bd.r;
-        chi[a] = bd.used[a] && g.phys_hi[a] && hi > g.n[a] + bd.r;
-        if (clo[a]) lo = -bd.r;
-        if (chi[a]) hi = g.n[a] + bd.r;
+        clo[a] = used[a] && g.phys_lo[a] && lo < -RR;
+        chi[a] = used[a] && g.phys_hi[a] && hi > g.n[a] + RR;
+        if (clo[a]) lo = -RR;
+        if (chi[a]) hi = g.n[a] + RR;
         ilo[a] = lo;
         ie[a] = hi - lo;
     }
-    const int vol = ie[0] * ie[1] * ie[2];
+    const int S1 = ie[2], S0 = ie[1] * ie[2];
     T* cur = smem;
-    T* nxt = smem + vol;
+    T* nxt = smem + ie[0] * S0;
     const long long s0 = g.stride0, s1 = g.stride1;
-    for (int e = tid; e < vol; e += nthr) {
-        const int c2 = e % ie[2], c1 = (e / ie[2]) % ie[1], c0 = e / (ie[2] * ie[1]);
-        const long long a0 = g.origin[0] + ilo[0] + c0, a1 = g.origin[1] + ilo[1] + c1, a2 = g.origin[2] + ilo[2] + c2;
-        T v = T(0);
-        if (a0 >= 0 && a0 < g.ext[0] && a1 >= 0 && a1 < g.ext[1] && a2 >= 0 && a2 < g.ext[2]) v = src[a0 * s0 + a1 * s1 + a2];
-        cur[e] = v;
-    }
+    band_rows<C>(ie[0], ie[1], ie[2], tid, nthr, [&](int c0, int c1, int lx, int LX) {
+        const long long a0 = g.origin[0] + ilo[0] + c0, a1 = g.origin[1] + ilo[1] + c1;
+        const bool rowin = a0 >= 0 && a0 < g.ext[0] && a1 >= 0 && a1 < g.ext[1];
+        const T* gp = src + a0 * s0 + a1 * s1 + g.origin[2] + ilo[2];
+        T* sp = cur + c0 * S0 + c1 * S1;
+        for (int c2 = lx; c2 < ie[2]; c2 += LX) {
+            const long long a2 = g.origin[2] + ilo[2] + c2;
+            sp[c2] = (rowin && a2 >= 0 && a2 < g.ext[2]) ? gp[c2] : T(0);
+        }
+    });
     __syncthreads();
     for (int s = 1; s <= bd.m; ++s) {
         int rlo[3], re[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-            const int sh = bd.used[a] ? s * bd.r : 0;
+            const int sh = used[a] ? s * RR : 0;
             rlo[a] = clo[a] ? 0 : sh;
             re[a] = ie[a] - rlo[a] - (chi[a] ? 0 : sh);
         }
-        const int rvol = re[0] * re[1] * re[2];
-        for (int e = tid; e < rvol; e += nthr) {
-            const int c2 = e % re[2] + rlo[2], c1 = (e / re[2]) % re[1] + rlo[1], c0 = e / (re[2] * re[1]) + rlo[0];
-            const int q[3] = {ilo[0] + c0, ilo[1] + c1, ilo[2] + c2};
-            bool ring = false;
+        band_rows<C>(re[0], re[1], re[2], tid, nthr, [&](int d0, int d1, int lx, int LX) {
+            const int c0 = d0 + rlo[0], c1 = d1 + rlo[1];
+            const int q0 = ilo[0] + c0, q1 = ilo[1] + c1;
+            const bool rowring = (q0 < 0 && g.phys_lo[0]) || (q0 >= g.n[0] && g.phys_hi[0]) ||
+                                 (used[1] && ((q1 < 0 && g.phys_lo[1]) || (q1 >= g.n[1] && g.phys_hi[1])));
+            const int lrow = c0 * S0 + c1 * S1;
+            for (int d2 = lx; d2 < re[2]; d2 += LX) {
+                const int c2 = d2 + rlo[2], q2 = ilo[2] + c2;
+                const int li = lrow + c2;
+                T acc;
+                if (rowring || (q2 < 0 && g.phys_lo[2]) || (q2 >= g.n[2] && g.phys_hi[2])) {
+                    acc = cur[li];
+                } else {
+                    acc = T(0);
+                    int j = 0;
 #pragma unroll
-            for (int a = 0; a < 3; ++a)
-                if (bd.used[a] && ((q[a] < 0 && g.phys_lo[a]) || (q[a] >= g.n[a] && g.phys_hi[a]))) ring = true;
-            const int li = (c0 * ie[1] + c1) * ie[2] + c2;
-            T acc;
-            if (ring) {
-                acc = cur[li];
-            } else {
-                acc = T(0);
-                for (int j = 0; j < bd.ntaps; ++j)
-                    acc = fmaT(bd.w[j], cur[li + (bd.toff[j][0] * ie[1] + bd.toff[j][1]) * ie[2] + bd.toff[j][2]], acc);
+                    for (int o0 = -RR; o0 <= RR; ++o0)
+#pragma unroll
+                        for (int o1 = (used[1] ? -RR : 0); o1 <= (used[1] ? RR : 0); ++o1)
+#pragma unroll
+                            for (int o2 = -RR; o2 <= RR; ++o2) {
+                                if (!in_support<C::SHAPE, RR, 1>(o0, o1, o2)) continue;
+                                acc = fmaT(bd.w[j], cur[li + o0 * S0 + o1 * S1 + o2], acc);
+                                ++j;
+                            }
+                }
+                nxt[li] = acc;
             }
-            nxt[li] = acc;
-        }
+        });
         __syncthreads();
         T* tmp = cur;
         cur = nxt;
         nxt = tmp;
     }
-    const int oe1 = ohi[1] - olo[1], oe2 = ohi[2] - olo[2];
-    const int ovol = (ohi[0] - olo[0]) * oe1 * oe2;
-    for (int e = tid; e < ovol; e += nthr) {
-        const int c2 = e % oe2, c1 = (e / oe2) % oe1, c0 = e / (oe2 * oe1);
-        const int li = ((olo[0] - ilo[0] + c0) * ie[1] + (olo[1] - ilo[1] + c1)) * ie[2] + (olo[2] - ilo[2] + c2);
-        dst[(g.origin[0] + olo[0] + c0) * s0 + (g.origin[1] + olo[1] + c1) * s1 + g.origin[2] + olo[2] + c2] = cur[li];
-    }
+    const int oe0 = ohi[0] - olo[0], oe1 = ohi[1] - olo[1], oe2 = ohi[2] - olo[2];
+    band_rows<C>(oe0, oe1, oe2, tid, nthr, [&](int d0, int d1, int lx, int LX) {
+        const T* sp = cur + (olo[0] - ilo[0] + d0) * S0 + (olo[1] - ilo[1] + d1) * S1 + (olo[2] - ilo[2]);
+        T* gp = dst + (g.origin[0] + olo[0] + d0) * s0 + (g.origin[1] + olo[1] + d1) * s1 + g.origin[2] + olo[2];
+        for (int d2 = lx; d2 < oe2; d2 += LX) gp[d2] = sp[d2];
+    });
     __syncthreads();
 }
 
@@ -494,31 +574,45 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     const int tx = threadIdx.x % C::NTX, ty = threadIdx.x / C::NTX;
     // first computed column of this thread, relative to the tile's compute origin
     const int tcol = C::WARPSTAGE ? warp * C::WSTEP + lane * C::VX : tx * C::VX;
-    int off0[C::NV];
+    // shared-window byte address of this thread's first neighbourhood row in slot 0
+    // plus per-vector offsets (loop invariant, kept in registers)
+    const uint32_t sbase = pin(ptx::smem_u32(slots) + (uint32_t)(ty * C::VY * C::BX * (int)sizeof(T)));
+    uint32_t soff[C::NV];
 #pragma unroll
     for (int v = 0; v < C::NV; ++v) {
         const int c = tcol + v * C::VEC;
-        off0[v] = (c / C::BX) * C::CHUNK + (c % C::BX);
+        soff[v] = (uint32_t)(((c / C::BX) * C::CHUNK + (c % C::BX)) * (int)sizeof(T));
+    }
+    // folded coefficients lambda^(Q) in registers (only the support is referenced)
+    T cf[C::NC];
+#pragma unroll
+    for (int ci = 0; ci < C::NC; ++ci) {
+        const int ox = ci % (2 * C::RQ + 1) - C::RQ;
+        const int oy = C::ND == 3 ? (ci / (2 * C::RQ + 1)) % (2 * C::RQY + 1) - C::RQY : 0;
+        const int oz = C::ND == 3 ? ci / ((2 * C::RQ + 1) * (2 * C::RQY + 1)) - C::RQ : ci / (2 * C::RQ + 1) - C::RQ;
+        cf[ci] = in_support<C::SHAPE, C::RR, C::Q>(oz, oy, ox) ? (C::PINC ? pin(p.coef[ci]) : p.coef[ci]) : T(0);
     }
     Consumer<C> cs;
     const T* __restrict__ src = p.src;
     T* __restrict__ dst = p.dst;
     const long long s0 = p.g.stride0, s1 = p.g.stride1;
+    // frozen-ring z range: planes z < zlo_f or z >= zhi_f are physical ring
+    const int zlo_f = p.g.phys_lo[0] ? 0 : -(1 << 30), zhi_f = p.g.phys_hi[0] ? p.g.n[0] : (1 << 30);
     int gx = 0, gy = 0, xlo = 0, xhi = 0, ylo = 0, yhi = 0;
-    T* obase = dst;           // output pointer of (z = -origin0, gy, gx) for the current run
+    T* optr = dst;            // output pointer of plane z_in - H (advanced by s0 per plane)
     unsigned vmask = 0, ymask = 0;   // full-vector stores allowed / rows in range
     bool edge_xy = false;
     int z_first = 0, out_lo = 0, out_hi = 0;
     bool done = false;
-    int i = 0;
+    int i = 0, pl = 0, slot = 0;
+    uint32_t phase = 0;
 #pragma unroll 1
     while (!done) {
         auto step = [&](auto PHc) {
             constexpr int PH = decltype(PHc)::value;
             if (done) return;
-            const int sq = i / C::PB, pl = i % C::PB, slot = sq % C::NSLOT;
             if (pl == 0) {
-                ptx::mbar_wait(&full[slot], (sq / C::NSLOT) & 1);
+                ptx::mbar_wait(&full[slot], phase);
                 const SlotMeta m = meta[slot];
                 if (m.flags & META_END) {
                     done = true;
@@ -542,7 +636,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                         xlo = max(xlo, wlo);
                         xhi = min(xhi, wlo + C::WSTEP);
                     }
-                    obase = dst + (p.g.origin[1] + gy) * s1 + p.g.origin[2] + gx;
+                    optr = dst + (p.g.origin[0] + m.z_first - C::H) * s0 + (p.g.origin[1] + gy) * s1 +
+                           p.g.origin[2] + gx;
                     vmask = 0;
 #pragma unroll
                     for (int mm = 0; mm < C::VX / C::VEC; ++mm)
@@ -568,18 +663,18 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             const int z_in = z_first + pl;
             // ---------------- stage 0: level-0 plane from the TMA ring
             {
-                const T* base = slots + slot * C::SLOT_ELEMS + (pl * C::ROWS + ty * C::VY) * C::BX;
+                const uint32_t pbase = sbase + (uint32_t)((slot * C::SLOT_ELEMS + pl * C::ROWS * C::BX) * (int)sizeof(T));
+                cs.template fold_plane<0, PH>(cf, [&](int rr, T* row) {
 #pragma unroll
-                for (int rr = 0; rr < C::NR; ++rr)
-#pragma unroll
-                    for (int v = 0; v < C::NV; ++v) VecT<T>::ld(base + rr * C::BX + off0[v], &cs.nb[rr][v * C::VEC]);
+                    for (int v = 0; v < C::NV; ++v)
+                        VecT<T>::lds(pbase + (uint32_t)(rr * C::BX * (int)sizeof(T)) + soff[v], row + v * C::VEC);
+                });
                 if (pl == C::PB - 1) {
                     __syncwarp();
                     if (lane == 0) ptx::mbar_arrive(&empty[slot]);
                 }
-                cs.template fold_plane<0, PH>(p.coef);
             }
-            // ---------------- stages 1..S-1 through shared-memory planes
+            // ---------------- stages 1..S-1
             auto stage = [&](auto Jc) {
                 constexpr int J = decltype(Jc)::value;
                 constexpr int dn = pmod(PH - J * C::RQ, C::NW);
@@ -592,8 +687,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                         cs.acc[J - 1][dn][vy][vx] = T(0);
                     }
                 const int z = z_in - J * C::RQ;
-                const bool zface = (p.g.phys_lo[0] && z < 0) || (p.g.phys_hi[0] && z >= p.g.n[0]);
-                if (edge_xy || zface) {
+                if (edge_xy || z < zlo_f || z >= zhi_f) {
 #pragma unroll
                     for (int vy = 0; vy < C::VY; ++vy)
 #pragma unroll
@@ -619,32 +713,32 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                 if constexpr (C::WARPSTAGE) {
                     // neighbours from adjacent lanes (lanes 0/31 get values that only
                     // feed the warp's redundant edge columns)
+                    cs.template fold_plane<J, PH>(cf, [&](int, T* row) {
 #pragma unroll
-                    for (int j = 0; j < C::NV * C::VEC; ++j) {
-                        const int rel = j - C::PX;                       // column relative to gx
-                        const int d = rel >= 0 ? rel / C::VX : -((-rel + C::VX - 1) / C::VX);
-                        const int e = rel - d * C::VX;
-                        if (d == 0) cs.nb[0][j] = v[0][e];
-                        else if (d < 0) cs.nb[0][j] = __shfl_up_sync(0xffffffffu, v[0][e], -d);
-                        else cs.nb[0][j] = __shfl_down_sync(0xffffffffu, v[0][e], d);
-                    }
+                        for (int j = 0; j < C::NV * C::VEC; ++j) {
+                            const int rel = j - C::PX;                       // column relative to gx
+                            const int d = rel >= 0 ? rel / C::VX : -((-rel + C::VX - 1) / C::VX);
+                            const int e = rel - d * C::VX;
+                            if (d == 0) row[j] = v[0][e];
+                            else if (d < 0) row[j] = __shfl_up_sync(0xffffffffu, v[0][e], -d);
+                            else row[j] = __shfl_down_sync(0xffffffffu, v[0][e], d);
+                        }
+                    });
                 } else {
-                T* lp = lev + ((J - 1) * 2 + (i & 1)) * C::LEV_ELEMS;
+                    T* lp = lev + ((J - 1) * 2 + (i & 1)) * C::LEV_ELEMS;
 #pragma unroll
-                for (int vy = 0; vy < C::VY; ++vy)
+                    for (int vy = 0; vy < C::VY; ++vy)
 #pragma unroll
-                    for (int mm = 0; mm < C::VX / C::VEC; ++mm)
-                        VecT<T>::st(lp + (ty * C::VY + vy + C::RQY) * C::COLS + tcol + C::PX + mm * C::VEC,
-                                    &v[vy][mm * C::VEC]);
-                ptx::named_bar_sync(1, C::NCONS);
-                const T* base = lp + (ty * C::VY) * C::COLS + tcol;
+                        for (int mm = 0; mm < C::VX / C::VEC; ++mm)
+                            VecT<T>::st(lp + (ty * C::VY + vy + C::RQY) * C::COLS + tcol + C::PX + mm * C::VEC,
+                                        &v[vy][mm * C::VEC]);
+                    ptx::named_bar_sync(1, C::NCONS);
+                    const T* base = lp + (ty * C::VY) * C::COLS + tcol;
+                    cs.template fold_plane<J, PH>(cf, [&](int rr, T* row) {
 #pragma unroll
-                for (int rr = 0; rr < C::NR; ++rr)
-#pragma unroll
-                    for (int vv = 0; vv < C::NV; ++vv)
-                        VecT<T>::ld(base + rr * C::COLS + vv * C::VEC, &cs.nb[rr][vv * C::VEC]);
+                        for (int vv = 0; vv < C::NV; ++vv) VecT<T>::ld(base + rr * C::COLS + vv * C::VEC, row + vv * C::VEC);
+                    });
                 }
-                cs.template fold_plane<J, PH>(p.coef);
             };
             if constexpr (C::S > 1) stage(std::integral_constant<int, 1>{});
             if constexpr (C::S > 2) stage(std::integral_constant<int, 2>{});
@@ -655,11 +749,10 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                 constexpr int dn = pmod(PH - C::H, C::NW);
                 const int z = z_in - C::H;
                 if (z >= out_lo && z < out_hi) {
-                    T* orow = obase + (p.g.origin[0] + z) * s0;
 #pragma unroll
                     for (int vy = 0; vy < C::VY; ++vy) {
                         if (!(ymask & (1u << vy))) continue;
-                        T* op = orow + vy * s1;
+                        T* op = optr + vy * s1;
 #pragma unroll
                         for (int mm = 0; mm < C::VX / C::VEC; ++mm) {
                             if (vmask & (1u << mm)) {
@@ -674,16 +767,46 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                         }
                     }
                 }
+                optr += s0;
 #pragma unroll
                 for (int vy = 0; vy < C::VY; ++vy)
 #pragma unroll
                     for (int vx = 0; vx < C::VX; ++vx) cs.acc[C::S - 1][dn][vy][vx] = T(0);
             }
             ++i;
+            if (++pl == C::PB) {
+                pl = 0;
+                if (++slot == C::NSLOT) {
+                    slot = 0;
+                    phase ^= 1u;
+                }
+            }
         };
-        [&]<int... PHs>(std::integer_sequence<int, PHs...>) {
-            (step(std::integral_constant<int, PHs>{}), ...);
-        }(std::make_integer_sequence<int, C::NW>{});
+        if constexpr (C::ROT) {
+            step(std::integral_constant<int, 0>{});
+#pragma unroll
+            for (int s = 0; s < C::S; ++s) {
+                T t0[C::VY][C::VX];
+#pragma unroll
+                for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                    for (int vx = 0; vx < C::VX; ++vx) t0[vy][vx] = cs.acc[s][0][vy][vx];
+#pragma unroll
+                for (int k = 0; k + 1 < C::NW; ++k)
+#pragma unroll
+                    for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                        for (int vx = 0; vx < C::VX; ++vx) cs.acc[s][k][vy][vx] = cs.acc[s][k + 1][vy][vx];
+#pragma unroll
+                for (int vy = 0; vy < C::VY; ++vy)
+#pragma unroll
+                    for (int vx = 0; vx < C::VX; ++vx) cs.acc[s][C::NW - 1][vy][vx] = t0[vy][vx];
+            }
+        } else {
+            [&]<int... PHs>(std::integer_sequence<int, PHs...>) {
+                (step(std::integral_constant<int, PHs>{}), ...);
+            }(std::make_integer_sequence<int, C::NW>{});
+        }
     }
     }  // consumers
 
@@ -696,7 +819,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             __syncthreads();
             const int blk = s_blk;
             if (blk >= p.band.nblk_total) break;
-            band_block<T>(p.band, p.g, p.src, p.dst, blk, slots, threadIdx.x, C::NTHREADS);
+            band_block<C>(p.band, p.g, p.src, p.dst, blk, slots, threadIdx.x, C::NTHREADS);
         }
     }
 }
@@ -941,6 +1064,30 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
 #ifndef SB_3D_NSLOT
 #define SB_3D_NSLOT 4
 #endif
+#ifndef SB_3D_VY
+#define SB_3D_VY 2
+#endif
+#ifndef SB_3D_PB
+#define SB_3D_PB 1
+#endif
+#ifndef SB_3D_MINB
+#define SB_3D_MINB 2
+#endif
+#ifndef SB_2D_MINB
+#define SB_2D_MINB 2
+#endif
+#ifndef SB_PINC_2D
+#define SB_PINC_2D 0
+#endif
+#ifndef SB_PINC_3D
+#define SB_PINC_3D 0
+#endif
+#ifndef SB_ROT_2D
+#define SB_ROT_2D 0
+#endif
+#ifndef SB_ROT_3D
+#define SB_ROT_3D 0
+#endif
 #ifndef SB_2D_VXM_HEAVY
 #define SB_2D_VXM_HEAVY 2
 #endif
@@ -949,9 +1096,10 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
 template <int SHAPE, int Q>
 constexpr int vxm2() { return (SHAPE == STENCIL_BOX ? Q >= 2 : Q >= 4) ? SB_2D_VXM_HEAVY : 1; }
 template <typename T, int SHAPE, int Q, int S>
-using Cfg2 = Cfg<T, 2, SHAPE, 1, Q, S, SB_2D_NTX / vxm2<SHAPE, Q>(), 1, 1, SB_2D_PB, SB_2D_NSLOT, vxm2<SHAPE, Q>()>;
+using Cfg2 = Cfg<T, 2, SHAPE, 1, Q, S, SB_2D_NTX / vxm2<SHAPE, Q>(), 1, 1, SB_2D_PB, SB_2D_NSLOT, vxm2<SHAPE, Q>(),
+                 SB_2D_MINB, SB_ROT_2D, SB_PINC_2D>;
 template <typename T, int SHAPE, int Q, int S>
-using Cfg3 = Cfg<T, 3, SHAPE, 1, Q, S, 32, SB_3D_NTY, 2, 1, SB_3D_NSLOT>;
+using Cfg3 = Cfg<T, 3, SHAPE, 1, Q, S, 32, SB_3D_NTY, SB_3D_VY, SB_3D_PB, SB_3D_NSLOT, 1, SB_3D_MINB, SB_ROT_3D, SB_PINC_3D>;
 
 using LaunchFn = int (*)(Plan*, const SweepCall&);
 
