@@ -299,17 +299,44 @@ def run_ours(args):
     clocks = ClockSampler(gpu_index(local)) if rank == 0 else None
     time.sleep(0.3)
     # --- timed region (kernel events on, so the dominant kernel is timed live)
+    # 1D: a whole run is ~10 us of GPU work, shorter than the host's launch path,
+    # so each step replays a CUDA graph of the run (captured once, untimed); its
+    # kernel durations are then taken from a second, event-instrumented pass.
+    # (The 2D/3D sweeps are not graph-replayed: their persistent-CTA schedule
+    # is epoch-tagged per launch.)
+    use_graph = nd == 1 and world == 1
+    graph = None
+    if use_graph:
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(m, args.stages)
+        graph.replay()
+        torch.cuda.synchronize()
     plan.timing_reset()
-    plan.set_timing(True)
+    plan.set_timing(not use_graph)
     barrier()
     torch.cuda.synchronize()
     if clocks:
         clocks.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
+    flush = None
+    if 3 * L.bytes < 126e6:
+        # buffers smaller than L2: flush it before every step (outside the step's events)
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(args.steps)]
     e0.record(stream)
-    for _ in range(args.steps):
-        step(m, args.stages)
+    for j in range(args.steps):
+        if flush is not None:
+            flush.zero_()
+            evs[j][0].record(stream)
+        if graph is not None:
+            graph.replay()
+        else:
+            step(m, args.stages)
+        if flush is not None:
+            evs[j][1].record(stream)
         launches += plan.last_launches
     e1.record(stream)
     torch.cuda.synchronize()
@@ -317,7 +344,16 @@ def run_ours(args):
     if clocks:
         clocks.stop()
     plan.set_timing(False)
-    ms_step = allmax(e0.elapsed_time(e1) / args.steps)
+    if flush is not None:
+        ms_step = allmax(sum(x.elapsed_time(y) for x, y in evs) / args.steps)
+    else:
+        ms_step = allmax(e0.elapsed_time(e1) / args.steps)
+    if use_graph:
+        plan.set_timing(True)
+        for _ in range(args.steps):
+            step(m, args.stages)
+        torch.cuda.synchronize()
+        plan.set_timing(False)
     kmain, kband = plan.timing(0), plan.timing(1)
     plan.timing_reset()
     value = points * T / (ms_step * 1e-3) / 1e9          # whole job (global points)
@@ -378,6 +414,8 @@ def run_ours(args):
             "fma": {"achieved_tfma_s": fma_ach, "peak_tfma_s": fma_peak, "frac": frac_f},
             "launches": kmain["launches"], "avg_launch_ms": avg_ms, "bytes_per_launch": bytes_per_launch,
             "kernel_share_of_step": kmain["ms"] / (ms_step * args.steps) if ms_step > 0 else None,
+            "kernel_timing": "second event-instrumented pass (steps are graph replays)" if use_graph
+            else "live, inside the timed region",
             "band": {"ms": kband["ms"], "launches": kband["launches"]}}
     cl = clocks.summary() if clocks else {}
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -385,8 +423,12 @@ def run_ours(args):
             "scaling": "weak", "vs_baseline": None, "dtype": cfg["dtype"], "data": "synthetic",
             "config": {"workload": cfg["name"] + (" x%d rows (slab per GPU)" % world if world > 1 else ""),
                        "dims": dims, "T": T, "fold_m": m, "stages": args.stages or "auto",
-                       "l2": "inputs larger than L2 (%.0f MB per buffer vs 126 MB)" % (L.bytes / 1e6),
-                       "parallelism": "slab%d" % world if world > 1 else "single"},
+                       "l2": ("inputs larger than L2 (%.0f MB per buffer vs 126 MB)" % (L.bytes / 1e6)
+                              if flush is None else
+                              "L2 flushed before every step (256 MB write, outside the step's events): "
+                              "buffers are %.1f MB" % (L.bytes / 1e6)),
+                       "parallelism": "slab%d" % world if world > 1 else "single",
+                       "cuda_graph": use_graph},
             "gpu_launches": launches,
             "e2e": {"value": points * T / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
