@@ -50,7 +50,7 @@ extern "C" {
 typedef enum {
     STENCIL_OK = 0,
     STENCIL_EINVAL = -1,        /* bad argument (dims, radius, ncoeffs, fold_m<1, T<0, null, aliasing, misalignment) */
-    STENCIL_EUNSUPPORTED = -2,  /* valid request this build does not compile (e.g. PERIODIC on GPU, fold_m*r too large) */
+    STENCIL_EUNSUPPORTED = -2,  /* valid request this build does not compile (e.g. PERIODIC dist runs, fold_m*r too large) */
     STENCIL_ECUDA = -3,         /* CUDA runtime/driver error (message in stencil_last_error) */
     STENCIL_ENCCL = -4,         /* NCCL error or NCCL library not loadable */
     STENCIL_ENOMEM = -5         /* host allocation failed */
@@ -100,7 +100,11 @@ typedef struct {
  *            (R4).  Copied.
  *   dtype    storage + arithmetic type on the GPU.  Folded weights are computed
  *            in fp64 and rounded once to dtype.
- *   boundary FIXED (supported on GPU) or PERIODIC (EUNSUPPORTED at run time).
+ *   boundary FIXED: an r-wide frozen ring holding u0 (R1); PERIODIC
+ *            (SURVEY §8(f) NEXT-4): the layout carries a ghost ring of
+ *            STENCIL_MAX_FOLD * r cells per side on every axis, refilled from
+ *            the wrapped interior after every sweep (single-GPU runs only;
+ *            dist layouts/runs return EUNSUPPORTED).
  * Errors: EINVAL on any bad argument.
  */
 int stencil_plan_create(stencil_plan *plan, int ndim, const int64_t *dims, int radius,
@@ -144,7 +148,8 @@ int stencil_fill_random(stencil_plan plan, void *buf, uint64_t seed, void *strea
  * in, out, workspace: device buffers of the plan layout (workspace may be NULL
  *   when at most one sweep runs).  `out` is fully written, ring included.
  * Errors: EINVAL (T < 0, fold_m < 1, null/aliased/misaligned pointers),
- *   EUNSUPPORTED (PERIODIC; fold_m*r > STENCIL_MAX_FOLD), ECUDA.
+ *   EUNSUPPORTED (fold_m > STENCIL_MAX_FOLD), ECUDA.  PERIODIC plans need a
+ *   workspace for every T > 0 (`in` is copied into the ping-pong first).
  */
 int stencil_run(stencil_plan plan, const void *in, void *out, int64_t T, int fold_m,
                 void *workspace, void *stream);

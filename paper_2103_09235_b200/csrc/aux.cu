@@ -38,7 +38,7 @@ struct Params1D {
     const T* src;
     T* dst;
     long long origin, ext;
-    int n, r, m, TB, B, nwarps, force_step;
+    int n, r, m, TB, B, nwarps, force_step, wrap;
     T lam[K1_MAXC];   // lambda^(m), index o + m r
     T w[9];           // original taps, index o + r
 };
@@ -84,7 +84,7 @@ __device__ __forceinline__ void steps1d(T (&a)[V], T (&b)[V], const T* __restric
     }
 }
 
-template <typename T, int V, int RF, int RS>
+template <typename T, int V, int RF, int RS, bool WRAP>
 __global__ void __launch_bounds__(K1_THREADS) onchip1d_kernel(const __grid_constant__ Params1D<T> p) {
     if (blockIdx.x == 0 && threadIdx.x < 32) {   // ring + pads (never written by the steps)
         for (long long g = threadIdx.x; g < p.origin; g += 32) p.dst[g] = p.src[g];
@@ -101,11 +101,16 @@ __global__ void __launch_bounds__(K1_THREADS) onchip1d_kernel(const __grid_const
     T a[V], b[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) {
-        const long long g = p.origin + c0 + v;
-        a[v] = (g >= 0 && g < p.ext) ? p.src[g] : T(0);
+        int x = c0 + v;
+        if constexpr (WRAP) {   // PERIODIC: the window wraps around the interior
+            x %= p.n;
+            x = x < 0 ? x + p.n : x;
+        }
+        const long long g = p.origin + x;
+        a[v] = (WRAP || (g >= 0 && g < p.ext)) ? p.src[g] : T(0);
     }
-    const int band = (p.m - 1) * p.r;
-    const bool stepwise = p.force_step || ilo < band || x1 + H > p.n - band;
+    const int band = WRAP ? 0 : (p.m - 1) * p.r;
+    const bool stepwise = p.force_step || (!WRAP && (ilo < band || x1 + H > p.n - band));
     if (!stepwise) {
         steps1d<T, V, RF, false>(a, b, p.lam, p.TB / p.m, 0u);
         steps1d<T, V, RS, false>(a, b, p.w, p.TB % p.m, 0u);
@@ -113,7 +118,7 @@ __global__ void __launch_bounds__(K1_THREADS) onchip1d_kernel(const __grid_const
         unsigned frozen = 0;   // cells outside the interior keep u0 (ring; beyond it: never read by valid cells)
 #pragma unroll
         for (int v = 0; v < V; ++v)
-            if (c0 + v < 0 || c0 + v >= p.n) frozen |= 1u << v;
+            if (!WRAP && (c0 + v < 0 || c0 + v >= p.n)) frozen |= 1u << v;
         steps1d<T, V, RS, true>(a, b, p.w, p.TB, frozen);
     }
 #pragma unroll
@@ -127,43 +132,47 @@ template <typename T>
 using K1Fn = void (*)(Params1D<T>);
 
 // dispatch table over (V in {8, 16, 32}, RS = r in 1..4, m in 1..8); V >= m*r.
-template <typename T, int V, int RS, int M>
+template <typename T, int V, int RS, int M, bool WRAP>
 constexpr K1Fn<T> k1_entry() {
     constexpr int RF = RS * M;
-    if constexpr (RF <= V) return onchip1d_kernel<T, V, RF, RS>;
+    if constexpr (RF <= V) return onchip1d_kernel<T, V, RF, RS, WRAP>;
     else return nullptr;
 }
-template <typename T, int V, int RS, int... Ms>
+template <typename T, int V, int RS, bool WRAP, int... Ms>
 constexpr void k1_row(K1Fn<T>* row, std::integer_sequence<int, Ms...>) {
-    ((row[Ms] = k1_entry<T, V, RS, Ms + 1>()), ...);
+    ((row[Ms] = k1_entry<T, V, RS, Ms + 1, WRAP>()), ...);
 }
-template <typename T, int V>
+template <typename T, int V, bool WRAP>
 static K1Fn<T> k1_pick_v(int r, int m) {
     static K1Fn<T> tab[4][8] = {};
     static bool init = false;
     if (!init) {
-        k1_row<T, V, 1>(tab[0], std::make_integer_sequence<int, 8>{});
-        k1_row<T, V, 2>(tab[1], std::make_integer_sequence<int, 8>{});
-        k1_row<T, V, 3>(tab[2], std::make_integer_sequence<int, 8>{});
-        k1_row<T, V, 4>(tab[3], std::make_integer_sequence<int, 8>{});
+        k1_row<T, V, 1, WRAP>(tab[0], std::make_integer_sequence<int, 8>{});
+        k1_row<T, V, 2, WRAP>(tab[1], std::make_integer_sequence<int, 8>{});
+        k1_row<T, V, 3, WRAP>(tab[2], std::make_integer_sequence<int, 8>{});
+        k1_row<T, V, 4, WRAP>(tab[3], std::make_integer_sequence<int, 8>{});
         init = true;
     }
     if (r < 1 || r > 4 || m < 1 || m > 8) return nullptr;
     return tab[r - 1][m - 1];
 }
+// PERIODIC windows (WRAP) are compiled for V in {16, 32} only.
 template <typename T>
-static K1Fn<T> k1_pick(int V, int r, int m) {
-    return V == 8 ? k1_pick_v<T, 8>(r, m) : V == 16 ? k1_pick_v<T, 16>(r, m) : k1_pick_v<T, 32>(r, m);
+static K1Fn<T> k1_pick(int V, int r, int m, bool wrap) {
+    if (wrap) return V == 32 ? k1_pick_v<T, 32, true>(r, m) : k1_pick_v<T, 16, true>(r, m);
+    return V == 8 ? k1_pick_v<T, 8, false>(r, m) : V == 16 ? k1_pick_v<T, 16, false>(r, m)
+                                                           : k1_pick_v<T, 32, false>(r, m);
 }
 
 // Cells per lane: the smallest of {8, 16, 32} holding the fold radius; the
 // env var STENCIL_1D_V overrides it (tuning).
-int onchip1d_cells_per_lane(int r, int m) {
+int onchip1d_cells_per_lane(int r, int m, bool wrap) {
     static int forced = [] {
         const char* e = getenv("STENCIL_1D_V");
         return e ? atoi(e) : 0;
     }();
-    int v = r * m <= 8 ? 8 : r * m <= 16 ? 16 : 32;
+    int v = (r * m <= 8 && !wrap) ? 8 : r * m <= 16 ? 16 : 32;
+    if (wrap) return v;
     if ((forced == 8 || forced == 16 || forced == 32) && forced >= r * m) v = forced;
     return v;
 }
@@ -182,12 +191,13 @@ static int launch_1d_t(Plan* p, const void* src, void* dst, const Layout3* L, in
     prm.m = m;
     prm.TB = (int)TB;
     prm.force_step = force_step ? 1 : 0;
+    prm.wrap = L->wrap ? 1 : 0;
     const std::vector<double>& lam = folded(p, m);
     if ((int)lam.size() > K1_MAXC || (int)p->w.size() > 9) return set_error(STENCIL_EUNSUPPORTED, "1D fold too wide");
     for (size_t i = 0; i < lam.size(); ++i) prm.lam[i] = static_cast<T>(lam[i]);
     for (size_t i = 0; i < p->w.size(); ++i) prm.w[i] = static_cast<T>(p->w[i]);
-    const int V = onchip1d_cells_per_lane(p->r, m);
-    K1Fn<T> fn = k1_pick<T>(V, p->r, m);
+    const int V = onchip1d_cells_per_lane(p->r, m, L->wrap);
+    K1Fn<T> fn = k1_pick<T>(V, p->r, m, L->wrap);
     if (!fn) return set_error(STENCIL_EUNSUPPORTED, "1D kernel: r or fold_m out of range");
     prm.B = 32 * V - 2 * (int)TB * p->r;   // outputs per warp
     if (prm.B <= 0) return set_error(STENCIL_EINVAL, "1D kernel: too many steps per launch for the warp window");
@@ -241,6 +251,51 @@ int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void
             static_cast<const float*>(src), static_cast<float*>(dst), g, rows);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "ring_copy_kernel launch");
+    return 1;
+}
+
+// ============================================================== PERIODIC ghosts
+// Every ghost cell (within the allocation, outside the interior) takes the
+// value of its wrapped interior cell; one warp per allocation row.  Reads and
+// writes are disjoint (interior -> ghosts), so one launch fills edges and
+// corners alike.
+template <typename T>
+__global__ void wrap_fill_kernel(T* __restrict__ buf, DevGeom g, long long rows, int used0, int used1) {
+    long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= rows) return;
+    const int lane = threadIdx.x & 31;
+    const long long r0 = row / g.ext[1], r1 = row % g.ext[1];
+    const long long c0 = r0 - g.origin[0], c1 = r1 - g.origin[1];
+    auto wrapi = [](long long c, long long n) { long long w = c % n; return w < 0 ? w + n : w; };
+    const long long w0 = used0 ? wrapi(c0, g.n[0]) : 0, w1 = used1 ? wrapi(c1, g.n[1]) : 0;
+    const bool inside = (!used0 || (c0 >= 0 && c0 < g.n[0])) && (!used1 || (c1 >= 0 && c1 < g.n[1]));
+    const T* srow = buf + (g.origin[0] + w0) * g.stride0 + (g.origin[1] + w1) * g.stride1 + g.origin[2];
+    T* drow = buf + r0 * g.stride0 + r1 * g.stride1 + g.origin[2];
+    const long long xlo = -(long long)g.lo_valid[2], xhi = g.n[2] + (long long)g.hi_valid[2];
+    if (!inside) {
+        for (long long x = xlo + lane; x < xhi; x += 32) drow[x] = srow[wrapi(x, g.n[2])];
+    } else {
+        for (long long x = xlo + lane; x < 0; x += 32) drow[x] = srow[wrapi(x, g.n[2])];
+        for (long long x = g.n[2] + lane; x < xhi; x += 32) drow[x] = srow[wrapi(x, g.n[2])];
+    }
+}
+
+int launch_wrap_fill(Plan* p, void* buf, const Layout3* L, void* stream) {
+    DevGeom g;
+    fill_geom(*L, &g);
+    const int used0 = p->ndim >= 2, used1 = p->ndim == 3;
+    // rows of the ghost-extended frame only: axis-0/1 rows in [-G, n+G)
+    long long rows = L->ext[0] * L->ext[1];
+    int wpb = 8;
+    unsigned blocks = (unsigned)((rows + wpb - 1) / wpb);
+    if (p->dtype == STENCIL_F64)
+        wrap_fill_kernel<double><<<blocks, wpb * 32, 0, (cudaStream_t)stream>>>(static_cast<double*>(buf), g, rows,
+                                                                                used0, used1);
+    else
+        wrap_fill_kernel<float><<<blocks, wpb * 32, 0, (cudaStream_t)stream>>>(static_cast<float*>(buf), g, rows,
+                                                                               used0, used1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "wrap_fill_kernel launch");
     return 1;
 }
 

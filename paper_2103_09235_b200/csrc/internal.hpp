@@ -40,6 +40,7 @@ struct Layout3 {
     int64_t bytes = 0;
     int64_t gofs0 = 0;               // dist: global index of local plane 0
     int64_t gn[3] = {1, 1, 1};       // global interior extents
+    bool wrap = false;               // PERIODIC: ghosts hold the wrapped interior
 };
 
 // ------------------------------------------------------------------ plan
@@ -96,9 +97,11 @@ int launch_sweep(Plan* p, const SweepCall& c);
 
 // 1D on-chip multi-step kernel (K-G4): T steps (fold m) in one launch.
 int launch_1d(Plan* p, const void* src, void* dst, const Layout3* L, int64_t T, int m,
-              int stages_flag, void* stream);
-int onchip1d_cells_per_lane(int r, int m);   // V of the warp window (32*V cells)
+              int stages_flag, void* stream);   // PERIODIC (L->wrap): loads wrap around
+int onchip1d_cells_per_lane(int r, int m, bool wrap);   // V of the warp window (32*V cells)
 
+// PERIODIC: fill every ghost cell of buf from its wrapped interior cell.
+int launch_wrap_fill(Plan* p, void* buf, const Layout3* L, void* stream);
 // Copy every non-interior cell (ring, ghosts, pads) src -> dst (K-G5).
 int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void* stream);
 // K-G0 seeded field over the frame (global padded index).

@@ -167,20 +167,27 @@ Layout3 make_layout(const Plan* p, int rank, int nranks, int halo) {
     if (nd == 3) { g[0] = p->dims[0]; g[1] = p->dims[1]; g[2] = p->dims[2]; }
     for (int a = 0; a < 3; ++a) { L.gn[a] = g[a]; L.n[a] = g[a]; }
     bool used[3] = {nd >= 2, nd == 3, true};
+    // PERIODIC: a ghost ring of G = STENCIL_MAX_FOLD * r cells per side on every
+    // axis, refilled from the wrapped interior after every sweep (no physical
+    // face, so no band); FIXED: the frozen r-ring.
+    const bool per = p->boundary == STENCIL_BC_PERIODIC;
+    const int64_t G = per ? (int64_t)STENCIL_MAX_FOLD * p->r : p->r;
+    L.wrap = per;
     for (int a = 0; a < 3; ++a) {
         if (!used[a]) {
             L.phys_lo[a] = L.phys_hi[a] = 0;
             L.lo_valid[a] = L.hi_valid[a] = 0;
         } else {
-            L.lo_valid[a] = L.hi_valid[a] = p->r;
+            L.lo_valid[a] = L.hi_valid[a] = G;
+            if (per) L.phys_lo[a] = L.phys_hi[a] = 0;
         }
     }
     // x
-    L.origin[2] = round_up(p->r, al);
-    L.ext[2] = round_up(L.origin[2] + g[2] + p->r, al);
+    L.origin[2] = round_up(G, al);
+    L.ext[2] = round_up(L.origin[2] + g[2] + G, al);
     L.stride[2] = 1;
     // y
-    if (used[1]) { L.origin[1] = p->r; L.ext[1] = g[1] + 2 * p->r; }
+    if (used[1]) { L.origin[1] = G; L.ext[1] = g[1] + 2 * G; }
     else { L.origin[1] = 0; L.ext[1] = 1; }
     L.stride[1] = L.ext[2];
     // stream axis
@@ -188,12 +195,12 @@ Layout3 make_layout(const Plan* p, int rank, int nranks, int halo) {
         int64_t nloc = g[0] / nranks;
         L.n[0] = nloc;
         L.gofs0 = nloc * rank;
-        int64_t h = nranks > 1 ? halo : p->r;
-        if (h < p->r) h = p->r;
+        int64_t h = nranks > 1 ? halo : G;
+        if (h < G) h = G;
         L.origin[0] = h;
         L.ext[0] = nloc + 2 * h;
-        L.phys_lo[0] = rank == 0;
-        L.phys_hi[0] = rank == nranks - 1;
+        L.phys_lo[0] = !per && rank == 0;
+        L.phys_hi[0] = !per && rank == nranks - 1;
         L.lo_valid[0] = L.phys_lo[0] ? p->r : h;
         L.hi_valid[0] = L.phys_hi[0] ? p->r : h;
     } else {
@@ -328,6 +335,7 @@ int stencil_plan_layout_dist(stencil_plan plan, int rank, int nranks, int halo,
     if (!plan || !out) return set_error(STENCIL_EINVAL, "NULL argument");
     Plan* p = reinterpret_cast<Plan*>(plan);
     if (p->ndim < 2) return set_error(STENCIL_EUNSUPPORTED, "dist layouts need ndim >= 2");
+    if (p->boundary != STENCIL_BC_FIXED) return set_error(STENCIL_EUNSUPPORTED, "dist layouts need a FIXED boundary");
     if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(STENCIL_EINVAL, "bad rank/nranks");
     if (halo < p->r) return set_error(STENCIL_EINVAL, "halo must be >= radius");
     if (p->dims[0] % nranks) return set_error(STENCIL_EINVAL, "axis-0 extent not divisible by nranks");

@@ -163,7 +163,8 @@ static int check_run_args(Plan* p, const void* in, void* out, int64_t T, int m, 
     if (in == out || (ws && (ws == in || ws == out))) return set_error(STENCIL_EINVAL, "in, out and workspace must not alias");
     if (misaligned(in) || misaligned(out) || (ws && misaligned(ws)))
         return set_error(STENCIL_EINVAL, "buffers must be 128-byte aligned");
-    if (p->boundary != STENCIL_BC_FIXED) return set_error(STENCIL_EUNSUPPORTED, "PERIODIC is not implemented on the GPU");
+    if (p->boundary == STENCIL_BC_PERIODIC && (int64_t)m * p->r > (int64_t)STENCIL_MAX_FOLD * p->r)
+        return set_error(STENCIL_EUNSUPPORTED, "PERIODIC: fold_m * r beyond the ghost ring");
     return STENCIL_OK;
 }
 
@@ -173,7 +174,7 @@ static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t 
     // steps per launch: the warp window (32*V cells) keeps at least half of its
     // cells as outputs, i.e. a halo H = TB*r <= 8*V; a multiple of m
     // (STENCIL_1D_HMAX overrides the 8*V halo bound: tuning)
-    const int V = onchip1d_cells_per_lane(p->r, m);
+    const int V = onchip1d_cells_per_lane(p->r, m, L.wrap);
     static const int64_t hforce = [] {
         const char* e = getenv("STENCIL_1D_HMAX");
         return e ? (int64_t)atoll(e) : (int64_t)0;
@@ -204,6 +205,11 @@ static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t 
         if (rc < 0) return rc;
         launches += rc;
     }
+    if (L.wrap) {   // PERIODIC: out's ghosts = its wrapped interior
+        rc = launch_wrap_fill(p, out, &L, stream);
+        if (rc < 0) return rc;
+        launches += rc;
+    }
     p->last_launches = launches;
     return STENCIL_OK;
 }
@@ -225,6 +231,36 @@ int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages,
     rc = resolve_variant(p, m, stages, &v);
     if (rc) return rc;
     const int64_t nf = T / m, nr = T % m, n = nf + nr;
+    if (L.wrap) {
+        // PERIODIC (NEXT-4): copy `in` (never written) into the buffer the
+        // ping-pong starts from, fill its ghosts from the wrapped interior, then
+        // after every sweep refill the ghosts of its output.  No band: there is
+        // no physical face, so lambda^(m) is valid everywhere.
+        if (!ws) return set_error(STENCIL_EINVAL, "workspace required for PERIODIC runs");
+        void* bufs[2] = {out, ws};
+        void* start = bufs[n % 2];   // so that sweep n writes `out`
+        cudaError_t e = cudaMemcpyAsync(start, in, L.bytes, cudaMemcpyDeviceToDevice, st);
+        if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync");
+        int launches = 0;
+        rc = launch_wrap_fill(p, start, &L, stream);
+        if (rc < 0) return rc;
+        launches += rc;
+        for (int64_t j = 1; j <= n; ++j) {
+            SweepSpec s;
+            s.m = j <= nf ? m : 1;
+            s.v = j <= nf ? v : Variant{1, 1};
+            const void* src = bufs[(n - j + 1) % 2];
+            void* dst = bufs[(n - j) % 2];
+            rc = enqueue_sweep(p, L, src, dst, s, 0, L.n[0], stream);
+            if (rc < 0) return rc;
+            launches += rc;
+            rc = launch_wrap_fill(p, dst, &L, stream);
+            if (rc < 0) return rc;
+            launches += rc;
+        }
+        p->last_launches = launches;
+        return STENCIL_OK;
+    }
     if (n >= 2 && !ws) return set_error(STENCIL_EINVAL, "workspace required when more than one sweep runs");
     int launches = 0;
     rc = launch_ring_copy(p, in, out, &L, stream);
@@ -314,6 +350,7 @@ struct Exchange {
 
 static int dist_layout_check(Plan* p, int rank, int nranks, int halo, int m, Layout3* L) {
     if (p->ndim < 2) return set_error(STENCIL_EUNSUPPORTED, "dist runs need ndim >= 2");
+    if (p->boundary != STENCIL_BC_FIXED) return set_error(STENCIL_EUNSUPPORTED, "dist runs need a FIXED boundary");
     if (p->dims[0] % nranks) return set_error(STENCIL_EINVAL, "axis-0 extent not divisible by nranks");
     if (halo < m * p->r) return set_error(STENCIL_EINVAL, "halo must be >= fold_m * radius");
     if (nranks > 1 && p->dims[0] / nranks < halo) return set_error(STENCIL_EINVAL, "slab thinner than the halo");

@@ -1,0 +1,103 @@
+#pragma once
+#include "sweep_impl.cuh"
+
+namespace sb {
+
+// sweep_cfg.cuh — tile configurations of the sweep kernel per (dim, shape, q, stages, r)
+// Tile configurations:
+//  2D: one row of NTX threads x VX (= 16 B) columns; PB rows per TMA slot.
+//  3D: NTX x NTY threads, each 2 x VY outputs, one plane per TMA slot.
+#ifndef SB_2D_NTX
+#define SB_2D_NTX 256
+#endif
+#ifndef SB_2D_PB
+#define SB_2D_PB 4
+#endif
+#ifndef SB_2D_NSLOT
+#define SB_2D_NSLOT 6
+#endif
+#ifndef SB_3D_NTY
+#define SB_3D_NTY 8
+#endif
+#ifndef SB_3D_NSLOT
+#define SB_3D_NSLOT 4
+#endif
+#ifndef SB_3D_VY
+#define SB_3D_VY 2
+#endif
+#ifndef SB_3D_PB
+#define SB_3D_PB 1
+#endif
+#ifndef SB_3D_MINB
+#define SB_3D_MINB 2
+#endif
+#ifndef SB_2D_MINB
+#define SB_2D_MINB 2
+#endif
+#ifndef SB_PINC_2D
+#define SB_PINC_2D 0
+#endif
+#ifndef SB_PINC_3D
+#define SB_PINC_3D 0
+#endif
+#ifndef SB_ROT_2D
+#define SB_ROT_2D 0
+#endif
+#ifndef SB_ROT_3D
+#define SB_ROT_3D 0
+#endif
+#ifndef SB_2D_VXM_HEAVY
+#define SB_2D_VXM_HEAVY 2
+#endif
+// FMA-heavy passes (|supp lambda^(Q)| >= 25) give each thread more outputs so the
+// neighbourhood loads and per-row bookkeeping are amortised over more FMAs.
+#ifndef SB_STAR_HEAVY_Q
+#define SB_STAR_HEAVY_Q 4
+#endif
+template <int SHAPE, int Q, int RR = 1>
+constexpr int vxm2() { return (SHAPE == STENCIL_BOX ? Q * RR >= 2 : Q * RR >= SB_STAR_HEAVY_Q) ? SB_2D_VXM_HEAVY : 1; }
+// light (VXM = 1) and heavy (VXM > 1) 2D passes: consumer threads, resident CTAs per SM
+#ifndef SB_2D_NTXH
+#define SB_2D_NTXH 128
+#endif
+#ifndef SB_2D_MINBH
+#define SB_2D_MINBH 2
+#endif
+#ifndef SB_2D_NSLOTH
+#define SB_2D_NSLOTH 6
+#endif
+#ifndef SB_2D_NSLOT_PLC
+#define SB_2D_NSLOT_PLC 4
+#endif
+// Window periods of at most 5 planes (Q <= 2) use one-period TMA slots (PB = NW,
+// branch-free phase loop; measured +7% on C3 m=2, +14% on C2 m=4 in 2 passes);
+// the 9-plane window of Q = 4 keeps 4-row slots (a 9-row slot would cost
+// occupancy and spill).
+template <int Q, int RR = 1>
+constexpr bool plc2() { return 2 * Q * RR + 1 <= 5; }
+template <typename T, int SHAPE, int Q, int S, int RR = 1>
+using Cfg2 = Cfg<T, 2, SHAPE, RR, Q, S, (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NTXH : SB_2D_NTX), 1, 1,
+                 (plc2<Q, RR>() ? 0 : SB_2D_PB),
+                 (plc2<Q, RR>() ? SB_2D_NSLOT_PLC : vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NSLOTH : SB_2D_NSLOT),
+                 vxm2<SHAPE, Q, RR>(), (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_MINBH : SB_2D_MINB), SB_ROT_2D, SB_PINC_2D>;
+// The folded 3D star pass with Q = 2 (25 taps, C4 m=2) takes 4 output rows per
+// thread (more FMAs per shared-memory row), 2-plane slots and pinned
+// coefficients (measured 514 vs 458 GStencil/s); the rest use the defaults.
+template <int SHAPE, int Q, int S>
+constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
+// (radius-2 3D configs use the defaults: star2_3d is keyed on Q only for r = 1)
+template <typename T, int SHAPE, int Q, int S, int RR = 1>
+using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32, (star2_3d<SHAPE, Q, S>() ? 4 : SB_3D_NTY),
+                 (star2_3d<SHAPE, Q, S>() ? 4 : SB_3D_VY), (star2_3d<SHAPE, Q, S>() ? 2 : SB_3D_PB),
+                 (star2_3d<SHAPE, Q, S>() ? 3 : SB_3D_NSLOT), 1, (star2_3d<SHAPE, Q, S>() ? 3 : SB_3D_MINB),
+                 SB_ROT_3D, (star2_3d<SHAPE, Q, S>() ? 1 : SB_PINC_3D)>;
+
+
+using LaunchFn = int (*)(Plan*, const SweepCall&);
+
+// Per-TU pickers (sweep_2d.cu, sweep_3d.cu, sweep_r2.cu)
+LaunchFn pick_2d(int dtype, int shape, int q, int s);
+LaunchFn pick_3d(int dtype, int shape, int q, int s);
+LaunchFn pick_r2(int dtype, int nd, int shape, int q, int s);
+
+}  // namespace sb

@@ -112,3 +112,20 @@ def test_dist_layout():
     L3 = p.layout_dist(3, 4, 2)
     assert L0.interior[0] == 16 and L0.origin[0] == 2 and L0.extent[0] == 20
     assert L3.global_offset0 == 48
+
+
+def test_periodic_layout_has_ghost_ring():
+    """PERIODIC plans (NEXT-4): a ghost ring of STENCIL_MAX_FOLD * r cells on
+    every axis (refilled from the wrapped interior after every sweep)."""
+    for r in (1, 2):
+        k = len(oracle.taps(2, r, oracle.BOX))
+        p = Plan((40, 30), r, "box", synth.weights(k, 1), boundary="periodic")
+        L = p.layout
+        G = 8 * r
+        assert L.origin[0] == G and L.extent[0] == 40 + 2 * G
+        assert L.origin[1] >= G and L.extent[1] >= L.origin[1] + 30 + G
+        assert (L.origin[1] * L.elem_bytes) % 128 == 0
+        # the frame view (interior + r-ring) still has the oracle's shape
+        assert tuple(p.frame_view(p.empty("cpu")).shape) == (40 + 2 * r, 30 + 2 * r)
+    with pytest.raises(StencilError):
+        Plan((64, 32), 1, "star", synth.weights(5, 1), boundary="periodic").layout_dist(0, 2, 2)

@@ -193,3 +193,38 @@ def test_errors_and_launch_count():
     plan.run(a, b, 8, 2, workspace=plan.empty())
     torch.cuda.synchronize()
     assert plan.last_launches >= 4 + 1
+
+
+def run_case_r(dims, r, shape, dtype, T, m, stages, boundary="fixed"):
+    """As run_case, for any radius (NEXT-4: higher-order stencils, e.g. 1D5P)."""
+    from paper_2103_09235_b200 import Plan
+    nd = len(dims)
+    offs = oracle.taps(nd, r, oracle.STAR if shape == "star" else oracle.BOX)
+    w = synth.weights(len(offs), 1)
+    u0 = synth.u0_frame(dims, r, 2)
+    bc = oracle.PERIODIC if boundary == "periodic" else oracle.FIXED
+    ref = oracle.run(dims, r, offs, w, u0, T, boundary=bc)
+    plan = Plan(dims, r, shape, w, dtype, boundary=boundary)
+    a = plan.from_frame(u0)
+    b, ws = plan.empty(), plan.empty()
+    plan.run(a, b, T, m, workspace=ws, stages=stages)
+    torch.cuda.synchronize()
+    got = plan.frame_view(b).cpu().double().numpy()
+    if boundary == "periodic":
+        sl = tuple(slice(r, -r) for _ in dims)
+        got, ref = got[sl], ref[sl]
+    return got, ref, u0
+
+
+@pytest.mark.parametrize("dims,shape,m,stages", [
+    ((5000,), "star", 1, 1), ((5000,), "star", 2, 1), ((5000,), "star", 4, 1), ((5000,), "star", 2, 2),
+    ((60, 301), "star", 1, 1), ((60, 301), "star", 2, 1), ((60, 301), "star", 2, 2),
+    ((60, 301), "box", 1, 1), ((60, 301), "box", 2, 1), ((60, 301), "box", 2, 2),
+    ((14, 23, 70), "star", 1, 1), ((14, 23, 70), "star", 2, 1), ((14, 23, 70), "star", 2, 2),
+    ((14, 23, 70), "box", 1, 1)])
+@pytest.mark.parametrize("dtype", ["f64", "f32"])
+@pytest.mark.parametrize("boundary", ["fixed", "periodic"])
+def test_parity_radius2(dims, shape, m, stages, dtype, boundary):
+    got, ref, u0 = run_case_r(dims, 2, shape, dtype, 6, m, stages, boundary)
+    err = np.max(np.abs(got - ref))
+    assert err <= TOL[dtype] * np.max(np.abs(u0)), err

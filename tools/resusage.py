@@ -23,7 +23,7 @@ for lib in libs:
             if c:
                 args = re.findall(r"Li(-?\d+)E", c.group(2))
                 names = ["Q", "S", "NTX", "NTY", "VY", "PB", "NSLOT", "VXM", "MINB", "ROT", "PINC"]
-                short = "%s nd=%s %s " % (c.group(1), args[0], "box" if args[1] == "1" else "star") + " ".join(
+                short = "%s nd=%s %s r=%s " % (c.group(1), args[0], "box" if args[1] == "1" else "star", args[2]) + " ".join(
                     "%s=%s" % kv for kv in zip(names, args[3:]))
             else:
                 short = re.sub(r"_ZN2sb\d+", "", name)[:60]

@@ -2,7 +2,7 @@
 
   python tools/tunebuild.py NAME -DSB_3D_VY=4 -DSB_3D_NTY=4 ...
 
-Recompiles sweep.cu with the extra defines, links it with the in-tree objects
+Recompiles the sweep*.cu sources with the extra defines, links it with the in-tree objects
 of the other sources and writes tunelibs/lib_NAME.so (load it with
 STENCIL_B200_LIB=... to measure a variant; tunelibs/ is scratch, git-ignored).
 """
@@ -20,10 +20,14 @@ def main():
     B.build()
     out = os.path.join(ROOT, "tunelibs")
     os.makedirs(out, exist_ok=True)
-    obj = os.path.join(out, "sweep_%s.o" % name)
-    cmd = [B.NVCC] + B.ARCH + B.FLAGS + defs + ["-c", os.path.join(B.CSRC, "sweep.cu"), "-o", obj]
-    subprocess.run(cmd, check=True)
-    objs = [obj] + [os.path.join(B.BUILD, s + ".o") for s in B.SOURCES if s != "sweep.cu"]
+    tuned = [f for f in B.SOURCES if f.startswith("sweep")]
+    objs = []
+    for src in tuned:
+        obj = os.path.join(out, "%s_%s.o" % (src[:-3], name))
+        cmd = [B.NVCC] + B.ARCH + B.FLAGS + defs + ["-c", os.path.join(B.CSRC, src), "-o", obj]
+        subprocess.run(cmd, check=True)
+        objs.append(obj)
+    objs += [os.path.join(B.BUILD, s + ".o") for s in B.SOURCES if s not in tuned]
     lib = os.path.join(out, "lib_%s.so" % name)
     subprocess.run([B.NVCC] + B.ARCH + ["-shared", "-cudart", "static", "-o", lib] + objs + ["-ldl"], check=True)
     print(lib)
