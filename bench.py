@@ -49,10 +49,23 @@ CONFIGS = {
                ms=(1, 2), best_m=2),
     "c5": dict(name="3D27P box fp64 768x768x384 T=100", dims=(384, 768, 768), shape="box", dtype="f64", T=100,
                ms=(1, 2), best_m=1),
+    # not a BASELINE config: C3's domain with the UNIFORM 2D9P weights of the paper's
+    # worked example -- lambda^(m) has rank 1, so the plan evaluates it
+    # through one counterpart (NEXT-3): 2*(2m+1) FMAs per point instead of (2m+1)^2
+    "c3u": dict(name="2D9P box fp32 uniform weights 16384x16384 T=200 (counterparts)", dims=(16384, 16384),
+                shape="box", dtype="f32", T=200, ms=(1, 2, 4), best_m=4, weights="uniform"),
 }
 SAMPLE = {  # oracle sub-window of each workload for the CPU baseline / reference arm
     "c1": (100000,), "c2": (1024, 1024), "c3": (1024, 1024), "c4": (96, 96, 96), "c5": (64, 64, 64),
+    "c3u": (1024, 1024),
 }
+
+
+def config_weights(cfg, k):
+    import synth
+    if cfg.get("weights") == "uniform":
+        return [1.0 / k] * k
+    return synth.weights(k, synth.DEFAULT_SEED_W)
 
 
 def env_int(k, d):
@@ -152,7 +165,7 @@ def oracle_sample_run(cfg_key, target_s):
     nd = len(dims)
     sub = SAMPLE[cfg_key]
     offs = oracle.taps(nd, 1, oracle.STAR if cfg["shape"] == "star" else oracle.BOX)
-    w = synth.weights(len(offs), synth.DEFAULT_SEED_W)
+    w = config_weights(cfg, len(offs))
     lo = [(n - s) // 2 for n, s in zip(dims, sub)]
     u0 = synth.u0_block(dims, 1, lo, [l + s + 2 for l, s in zip(lo, sub)], synth.DEFAULT_SEED_U)
     t = time.perf_counter()
@@ -235,7 +248,7 @@ def run_ours(args):
     else:
         ms = [args.fold_m] if args.fold_m else list(cfg["ms"])
     k = {(1, "star"): 3, (2, "star"): 5, (2, "box"): 9, (3, "star"): 7, (3, "box"): 27}[(nd, cfg["shape"])]
-    w = synth.weights(k, synth.DEFAULT_SEED_W)
+    w = config_weights(cfg, k)
     plan = Plan(dims, 1, cfg["shape"], w, cfg["dtype"])
     T = cfg["T"]
     halo = max(ms)
@@ -428,7 +441,9 @@ def run_ours(args):
                               "L2 flushed before every step (256 MB write, outside the step's events): "
                               "buffers are %.1f MB" % (L.bytes / 1e6)),
                        "parallelism": "slab%d" % world if world > 1 else "single",
-                       "cuda_graph": use_graph},
+                       "cuda_graph": use_graph,
+                       "evaluation": dict(zip(("q", "stages", "counterparts"), plan.variant(m)))
+                       if args.stages == 0 and nd >= 2 else {"stages": args.stages or "auto"}},
             "gpu_launches": launches,
             "e2e": {"value": points * T / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},

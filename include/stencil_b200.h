@@ -46,6 +46,8 @@ extern "C" {
 
 #define STENCIL_MAX_DIMS 3
 #define STENCIL_MAX_FOLD 8
+/* Largest counterpart count (rank) the 2D counterpart evaluation is compiled for. */
+#define STENCIL_MAX_COUNTERPARTS 2
 
 typedef enum {
     STENCIL_OK = 0,
@@ -126,6 +128,38 @@ int stencil_plan_taps(stencil_plan plan, int *offsets, int cap);
  * Errors: EINVAL if m < 1 or cap too small; EUNSUPPORTED if m > STENCIL_MAX_FOLD.
  */
 int stencil_plan_fold_coeffs(stencil_plan plan, int m, double *dense, int64_t cap);
+
+/*
+ * Counterpart decomposition of the 2D folded weights (
+ * vertical/horizontal folding Eq.4-6, counterpart reuse Eq.7
+ * P:443-466).  Lambda = lambda^(m) viewed as a W x W matrix (W = 2 m r + 1,
+ * rows = offset along axis 0, columns = offset along x) is written as
+ *   Lambda[i][j] = sum_{k < rank} a[k W + i] * b[k W + j]
+ * by LU with complete pivoting, stopped when the largest residual entry is
+ * <= 1e-13 max|Lambda|.  The paper's uniform 2D9P, m = 2 example has rank 1
+ * (P:387).  When 2 W rank < |supp Lambda| and rank <=
+ * STENCIL_MAX_COUNTERPARTS, stencil_run evaluates the folded pass through the
+ * counterparts: each loaded row is folded horizontally with every b_k, and the
+ * counterparts are folded vertically with the a_k into the sliding window.
+ * rank: out; a, b: caller arrays of `cap` >= rank * W doubles (either may be
+ * NULL).  Errors: EINVAL (m < 1, NULL rank, cap too small), EUNSUPPORTED
+ * (ndim != 2, m > STENCIL_MAX_FOLD).
+ */
+int stencil_plan_fold_rank(stencil_plan plan, int m, int *rank, double *a, double *b, int64_t cap);
+
+/*
+ * Enable (default) or disable the counterpart evaluation for this plan
+ * (disabling forces the dense folded pass; used to compare the two).
+ */
+int stencil_plan_set_counterparts(stencil_plan plan, int enable);
+
+/*
+ * The evaluation stencil_run(..., fold_m = m, stages = 0) chooses for the
+ * main region (the GPU form of the profitability index Eq.3):
+ * `stages` passes of lambda^(q) (m = q * stages); rank > 0 = one pass through
+ * `rank` counterparts.  Errors: EINVAL (NULL, m < 1), EUNSUPPORTED (m too large).
+ */
+int stencil_plan_variant(stencil_plan plan, int m, int *q, int *stages, int *rank);
 
 /* Workspace bytes stencil_run needs (one more buffer of the plan's layout). */
 int stencil_workspace_size(stencil_plan plan, int64_t *bytes);

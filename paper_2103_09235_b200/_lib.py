@@ -32,6 +32,10 @@ SIGNATURES = {
     "stencil_plan_ntaps": (c_int, [c_vp, ctypes.POINTER(c_int)]),
     "stencil_plan_taps": (c_int, [c_vp, ctypes.POINTER(c_int), c_int]),
     "stencil_plan_fold_coeffs": (c_int, [c_vp, c_int, c_dp, c_i64]),
+    "stencil_plan_fold_rank": (c_int, [c_vp, c_int, ctypes.POINTER(c_int), c_dp, c_dp, c_i64]),
+    "stencil_plan_set_counterparts": (c_int, [c_vp, c_int]),
+    "stencil_plan_variant": (c_int, [c_vp, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int),
+                                     ctypes.POINTER(c_int)]),
     "stencil_workspace_size": (c_int, [c_vp, ctypes.POINTER(c_i64)]),
     "stencil_fill_random": (c_int, [c_vp, c_vp, c_u64, c_vp]),
     "stencil_run": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp]),

@@ -124,6 +124,27 @@ class Plan:
                                                  out.size))
         return out
 
+    def fold_rank(self, m: int):
+        """Counterpart decomposition of lambda^(m) (2D): (rank, a, b) with
+        lambda^(m)[i, j] = sum_k a[k, i] b[k, j] (stencil_plan_fold_rank)."""
+        W = 2 * m * self.radius + 1
+        rank = ctypes.c_int()
+        a = np.zeros((W, W), dtype=np.float64)
+        b = np.zeros((W, W), dtype=np.float64)
+        check(self._lib.stencil_plan_fold_rank(self._h, int(m), ctypes.byref(rank),
+                                               a.ctypes.data_as(ctypes.POINTER(ctypes.c_double)),
+                                               b.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), a.size))
+        return rank.value, a[:rank.value].copy(), b[:rank.value].copy()
+
+    def set_counterparts(self, enable: bool) -> None:
+        check(self._lib.stencil_plan_set_counterparts(self._h, 1 if enable else 0))
+
+    def variant(self, m: int):
+        """(q, stages, rank) the plan chooses for fold_m = m (stencil_plan_variant)."""
+        q, s, r = ctypes.c_int(), ctypes.c_int(), ctypes.c_int()
+        check(self._lib.stencil_plan_variant(self._h, int(m), ctypes.byref(q), ctypes.byref(s), ctypes.byref(r)))
+        return q.value, s.value, r.value
+
     def layout_dist(self, rank: int, nranks: int, halo: int) -> Layout:
         cl = StencilLayout()
         check(self._lib.stencil_plan_layout_dist(self._h, rank, nranks, halo, ctypes.byref(cl)))

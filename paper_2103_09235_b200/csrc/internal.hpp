@@ -55,10 +55,12 @@ struct Plan {
     std::vector<double> w;       // k weights (fp64)
     // folded maps lambda^(q) as dense (2qr+1)^ndim fp64, q = 1..STENCIL_MAX_FOLD
     std::map<int, std::vector<double>> lam;
+    std::map<int, struct LowRank*> lowrank;   // owned; 2D counterpart decompositions
     std::mutex mu;
     int64_t last_launches = 0;
     // measurement support (stencil_plan_set_timing)
     bool timing = false;
+    bool counterparts = true;     // stencil_plan_set_counterparts
     struct TimingRec { void* a; void* b; int kind; int64_t bytes; int64_t fmas; };
     std::vector<TimingRec> recs;
     std::vector<void*> event_pool;
@@ -75,8 +77,19 @@ Layout3 make_layout(const Plan* p, int rank, int nranks, int halo);
 void to_public(const Layout3& L, stencil_layout* out);
 
 // Evaluation variant of one m-step sweep on the main (folded-valid) region.
-struct Variant { int q; int stages; };
-Variant choose_variant(const Plan* p, int m);
+// rank > 0: the pass evaluates lambda^(q) through `rank` counterparts
+// (Eq.4-7): a horizontal fold per counterpart of every loaded row,
+// then the vertical fold of the counterparts into the window (2D only).
+struct Variant { int q; int stages; int rank = 0; };
+Variant choose_variant(Plan* p, int m);
+
+// Counterpart decomposition of the 2D folded matrix Lambda = lambda^(q)
+// (rows: vertical offset, columns: horizontal offset):
+//   Lambda = sum_k a_k b_k^T, k < rank,
+// by LU with complete pivoting, stopped when the largest residual entry is
+// below 1e-13 max|Lambda| (exact for the paper's rank-1 uniform example).
+struct LowRank { int rank = 0; int W = 0; std::vector<double> a, b; };   // a, b: rank x W
+const LowRank& lowrank(Plan* p, int q);
 int support_size(int ndim, int shape, int r, int q);
 
 // ------------------------------------------------------------------ kernels
@@ -88,7 +101,8 @@ struct SweepCall {
     const Layout3* L;
     std::vector<Box> boxes;   // output boxes (interior coords)
     int q, stages;
-    const std::vector<double>* coef;   // lambda^(q), dense fp64
+    const std::vector<double>* coef;   // lambda^(q), dense fp64 (or packed a_k | b_k when rank > 0)
+    int rank = 0;                      // counterpart evaluation (Variant::rank)
     std::vector<Box> band;    // exact stepwise band boxes (K-G3), same launch
     int band_m = 1;           // steps of the band (the sweep's fold_m)
     void* stream;

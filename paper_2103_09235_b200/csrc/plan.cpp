@@ -128,9 +128,53 @@ int support_size(int nd, int shape, int r, int q) {
 // 930 vs 664 GStencil/s), because the single pass needs no intermediate
 // hand-off; above that (2D9P m=4: 81 taps, 3D27P m=2: 125 taps) the divisor
 // split (q, stages) with the fewest FMAs per point wins.
-Variant choose_variant(const Plan* p, int m) {
+const LowRank& lowrank(Plan* p, int q) {
+    const std::vector<double>& lam = folded(p, q);   // (takes the plan lock itself)
+    std::lock_guard<std::mutex> g(p->mu);
+    auto it = p->lowrank.find(q);
+    if (it != p->lowrank.end()) return *it->second;
+    LowRank* lr = new LowRank();
+    p->lowrank[q] = lr;
+    if (p->ndim != 2) return *lr;
+    const int W = 2 * q * p->r + 1;
+    lr->W = W;
+    std::vector<double> R(lam);
+    double amax = 0.0;
+    for (double v : R) amax = std::max(amax, std::fabs(v));
+    for (int k = 0; k < W; ++k) {
+        int bi = 0, bj = 0;
+        double best = 0.0;
+        for (int i = 0; i < W; ++i)
+            for (int j = 0; j < W; ++j)
+                if (std::fabs(R[i * W + j]) > best) { best = std::fabs(R[i * W + j]); bi = i; bj = j; }
+        if (best <= 1e-13 * amax) break;
+        const double piv = R[bi * W + bj];
+        std::vector<double> a(W), b(W);
+        for (int i = 0; i < W; ++i) a[i] = R[i * W + bj];
+        for (int j = 0; j < W; ++j) b[j] = R[bi * W + j] / piv;
+        for (int i = 0; i < W; ++i)
+            for (int j = 0; j < W; ++j) R[i * W + j] -= a[i] * b[j];
+        lr->a.insert(lr->a.end(), a.begin(), a.end());
+        lr->b.insert(lr->b.end(), b.begin(), b.end());
+        ++lr->rank;
+    }
+    return *lr;
+}
+
+Variant choose_variant(Plan* p, int m) {
     if (m <= 1) return {1, 1};
     const int full = support_size(p->ndim, p->shape, p->r, m);
+    // GPU form of the profitability index (Eq.3): the counterpart
+    // evaluation costs rank * (W + W) FMAs per point (a horizontal fold per
+    // counterpart, then the vertical fold of the counterparts, Eq.4-6), the
+    // folded one |supp lambda^(m)|; take the counterparts when they are fewer
+    // and a compiled rank exists (the paper's uniform 2D9P, m=2: 10 vs 25).
+    if (p->ndim == 2 && p->r == 1 && p->counterparts && (m == 2 || m == 4)) {
+        const LowRank& lr = lowrank(p, m);
+        const int W = 2 * m * p->r + 1;
+        if (lr.rank >= 1 && lr.rank <= STENCIL_MAX_COUNTERPARTS && 2 * W * lr.rank < full)
+            return Variant{m, 1, lr.rank};
+    }
     if (full <= 64) return {m, 1};
     Variant best = {m, 1};
     double best_cost = 1e30;
@@ -287,6 +331,7 @@ int stencil_plan_destroy(stencil_plan plan) {
         }
         for (void* e : p->event_pool) cudaEventDestroy((cudaEvent_t)e);
         if (p->sched) cudaFree(p->sched);
+        for (auto& kv : p->lowrank) delete kv.second;
     }
     delete p;
     return STENCIL_OK;
@@ -321,6 +366,39 @@ int stencil_plan_fold_coeffs(stencil_plan plan, int m, double* dense, int64_t ca
     const std::vector<double>& lam = folded(p, m);
     if (cap < (int64_t)lam.size()) return set_error(STENCIL_EINVAL, "capacity too small");
     std::copy(lam.begin(), lam.end(), dense);
+    return STENCIL_OK;
+}
+
+int stencil_plan_fold_rank(stencil_plan plan, int m, int* rank, double* a, double* b, int64_t cap) {
+    if (!plan || !rank) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (m < 1) return set_error(STENCIL_EINVAL, "fold_m must be >= 1");
+    if (m > STENCIL_MAX_FOLD) return set_error(STENCIL_EUNSUPPORTED, "fold_m > STENCIL_MAX_FOLD");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (p->ndim != 2) return set_error(STENCIL_EUNSUPPORTED, "counterpart decomposition is 2D");
+    const LowRank& lr = lowrank(p, m);
+    *rank = lr.rank;
+    if (a || b) {
+        if (cap < (int64_t)lr.a.size()) return set_error(STENCIL_EINVAL, "capacity too small");
+        if (a) std::copy(lr.a.begin(), lr.a.end(), a);
+        if (b) std::copy(lr.b.begin(), lr.b.end(), b);
+    }
+    return STENCIL_OK;
+}
+
+int stencil_plan_set_counterparts(stencil_plan plan, int enable) {
+    if (!plan) return set_error(STENCIL_EINVAL, "NULL argument");
+    reinterpret_cast<Plan*>(plan)->counterparts = enable != 0;
+    return STENCIL_OK;
+}
+
+int stencil_plan_variant(stencil_plan plan, int m, int* q, int* stages, int* rank) {
+    if (!plan || !q || !stages || !rank) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (m < 1) return set_error(STENCIL_EINVAL, "fold_m must be >= 1");
+    if (m > STENCIL_MAX_FOLD) return set_error(STENCIL_EUNSUPPORTED, "fold_m > STENCIL_MAX_FOLD");
+    Variant v = choose_variant(reinterpret_cast<Plan*>(plan), m);
+    *q = v.q;
+    *stages = v.stages;
+    *rank = v.rank;
     return STENCIL_OK;
 }
 

@@ -109,7 +109,16 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
     if (!mb.empty()) sc.boxes.push_back(mb);
     sc.q = s.v.q;
     sc.stages = s.v.stages;
-    sc.coef = &folded(p, s.v.q);
+    sc.rank = s.v.rank;
+    std::vector<double> packed;
+    if (s.v.rank > 0) {   // counterparts: a_0..a_{rank-1} | b_0..b_{rank-1}
+        const LowRank& lr = lowrank(p, s.v.q);
+        packed.assign(lr.a.begin(), lr.a.begin() + (size_t)s.v.rank * lr.W);
+        packed.insert(packed.end(), lr.b.begin(), lr.b.begin() + (size_t)s.v.rank * lr.W);
+        sc.coef = &packed;
+    } else {
+        sc.coef = &folded(p, s.v.q);
+    }
     sc.stream = stream;
     if (s.m > 1) {
         for (const Box& b : band) {
@@ -122,9 +131,9 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
     {
         int64_t pts = mb.volume(), bpts = 0;
         for (const Box& b : sc.band) bpts += b.volume();
-        TimedScope ts(p, stream, 0, 2 * L.esize * (pts + bpts),
-                      pts * s.v.stages * support_size(p->ndim, p->shape, p->r, s.v.q) +
-                          bpts * s.m * (int64_t)p->w.size());
+        const int64_t per_pt = s.v.rank > 0 ? (int64_t)s.v.rank * 2 * (2 * s.v.q * p->r + 1)
+                                            : (int64_t)s.v.stages * support_size(p->ndim, p->shape, p->r, s.v.q);
+        TimedScope ts(p, stream, 0, 2 * L.esize * (pts + bpts), pts * per_pt + bpts * s.m * (int64_t)p->w.size());
         rc = launch_sweep(p, sc);
     }
     if (rc < 0) return rc;
@@ -134,8 +143,13 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
 
 static int resolve_variant(Plan* p, int m, int stages, Variant* v) {
     if (m == 1) { *v = {1, 1}; return STENCIL_OK; }
+    if (stages == 0 || stages == 1) {
+        Variant c = choose_variant(p, m);
+        if (c.rank > 0 && sweep_supported(p, c.q, 1, c.rank)) { *v = c; return STENCIL_OK; }   // one pass, counterparts
+    }
     if (stages == 0) {
         *v = choose_variant(p, m);
+        v->rank = 0;
         if (!sweep_supported(p, v->q, v->stages)) {
             // fall back to any compiled split of m
             for (int s = 1; s <= m; ++s)

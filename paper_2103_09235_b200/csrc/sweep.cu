@@ -12,10 +12,14 @@ static LaunchFn pick(int dtype, int nd, int shape, int r, int q, int s) {
     return nullptr;
 }
 
-bool sweep_supported(const Plan* p, int q, int s) { return pick(p->dtype, p->ndim, p->shape, p->r, q, s) != nullptr; }
+bool sweep_supported(const Plan* p, int q, int s, int rank) {
+    if (rank > 0) return s == 1 && p->ndim == 2 && p->r == 1 && pick_cp(p->dtype, q, rank) != nullptr;
+    return pick(p->dtype, p->ndim, p->shape, p->r, q, s) != nullptr;
+}
 
 int launch_sweep(Plan* p, const SweepCall& c) {
-    LaunchFn fn = pick(p->dtype, p->ndim, p->shape, p->r, c.q, c.stages);
+    LaunchFn fn = c.rank > 0 ? (p->ndim == 2 && p->r == 1 && c.stages == 1 ? pick_cp(p->dtype, c.q, c.rank) : nullptr)
+                             : pick(p->dtype, p->ndim, p->shape, p->r, c.q, c.stages);
     if (!fn)
         return set_error(STENCIL_EUNSUPPORTED, "no compiled sweep for ndim=" + std::to_string(p->ndim) +
                                                    " r=" + std::to_string(p->r) + " q=" + std::to_string(c.q) +

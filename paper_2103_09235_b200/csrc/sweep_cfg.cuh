@@ -93,11 +93,18 @@ using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32, (star2_3d<SHAPE, Q, S>() ? 4 : SB_3D
                  SB_ROT_3D, (star2_3d<SHAPE, Q, S>() ? 1 : SB_PINC_3D)>;
 
 
+// 2D counterpart passes (NEXT-3): one pass of lambda^(Q) through CP
+// counterparts; the tile of the light 2D passes (4 + 2*... FMAs per row-point).
+template <typename T, int Q, int CP>
+using Cfg2CP = Cfg<T, 2, STENCIL_BOX, 1, Q, 1, SB_2D_NTX, 1, 1, (plc2<Q>() ? 0 : SB_2D_PB),
+                   (plc2<Q>() ? SB_2D_NSLOT_PLC : SB_2D_NSLOT), 1, SB_2D_MINB, 0, 0, CP>;
+
 using LaunchFn = int (*)(Plan*, const SweepCall&);
 
 // Per-TU pickers (sweep_2d.cu, sweep_3d.cu, sweep_r2.cu)
 LaunchFn pick_2d(int dtype, int shape, int q, int s);
 LaunchFn pick_3d(int dtype, int shape, int q, int s);
 LaunchFn pick_r2(int dtype, int nd, int shape, int q, int s);
+LaunchFn pick_cp(int dtype, int q, int rank);
 
 }  // namespace sb

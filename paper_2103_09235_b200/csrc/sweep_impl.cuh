@@ -50,7 +50,7 @@ namespace sb {
 
 // ------------------------------------------------------------------ config
 template <typename T_, int ND_, int SHAPE_, int RR_, int Q_, int S_, int NTX_, int NTY_, int VY_, int PB_,
-          int NSLOT_, int VXM_ = 1, int MINB_ = 2, int ROT_ = 0, int PINC_ = 0>
+          int NSLOT_, int VXM_ = 1, int MINB_ = 2, int ROT_ = 0, int PINC_ = 0, int CP_ = 0>
 struct Cfg {
     using T = T_;
     static constexpr int ND = ND_, SHAPE = SHAPE_, RR = RR_, Q = Q_, S = S_;
@@ -100,6 +100,10 @@ struct Cfg {
     // kernel (otherwise the compiler may re-load them from the constant bank
     // every plane).
     static constexpr bool PINC = PINC_ != 0;
+    // CP > 0 (2D): the pass evaluates lambda^(Q) through CP counterparts
+    // (coef = a_0..a_{CP-1} | b_0..b_{CP-1}, each 2*RQ+1 long).
+    static constexpr int CP = CP_;
+    static_assert(CP == 0 || ND_ == 2, "counterpart evaluation is 2D");
     static constexpr int NC = ND == 3 ? NW * NW * NW : NW * NW;
     static constexpr size_t DATA_BYTES = (size_t)NSLOT * SLOT_ELEMS * sizeof(T) +
                                          (size_t)(S - 1) * 2 * LEV_ELEMS * sizeof(T);
@@ -192,6 +196,35 @@ struct Consumer {
     template <int J, int PH, class LD>
     __device__ __forceinline__ void fold_plane(const T (&coef)[C::NC], LD&& ld) {
         constexpr int RQ = C::RQ, RQY = C::RQY, NW = C::NW;
+        if constexpr (C::CP > 0) {
+            // Counterparts (Eq.4-7): fold the loaded row horizontally with every
+            // b_k (h_k = b_k (x) row), then fold the counterparts vertically into
+            // the window: pending output at stream offset oz gets sum_k a_k[oz] h_k.
+            constexpr int W = 2 * RQ + 1;
+            T row[C::NV * C::VEC];
+            ld(0, row);
+            T h[C::CP][C::VX];
+#pragma unroll
+            for (int k = 0; k < C::CP; ++k)
+#pragma unroll
+                for (int vx = 0; vx < C::VX; ++vx) {
+                    T s = T(0);
+#pragma unroll
+                    for (int ox = -RQ; ox <= RQ; ++ox) s = fmaT(coef[C::CP * W + k * W + ox + RQ], row[vx + ox + C::PX], s);
+                    h[k][vx] = s;
+                }
+#pragma unroll
+            for (int kk = 0; kk < NW; ++kk) {
+                const int oz = RQ - kk;
+                const int idx = pmod(PH - J * RQ - RQ + kk, NW);
+#pragma unroll
+                for (int k = 0; k < C::CP; ++k)
+#pragma unroll
+                    for (int vx = 0; vx < C::VX; ++vx)
+                        acc[J][idx][0][vx] = fmaT(coef[k * W + oz + RQ], h[k][vx], acc[J][idx][0][vx]);
+            }
+            return;
+        }
 #pragma unroll
         for (int rr = 0; rr < C::NR; ++rr) {
             T row[C::NV * C::VEC];
@@ -596,7 +629,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
         const int ox = ci % (2 * C::RQ + 1) - C::RQ;
         const int oy = C::ND == 3 ? (ci / (2 * C::RQ + 1)) % (2 * C::RQY + 1) - C::RQY : 0;
         const int oz = C::ND == 3 ? ci / ((2 * C::RQ + 1) * (2 * C::RQY + 1)) - C::RQ : ci / (2 * C::RQ + 1) - C::RQ;
-        cf[ci] = in_support<C::SHAPE, C::RR, C::Q>(oz, oy, ox) ? (C::PINC ? pin(p.coef[ci]) : p.coef[ci]) : T(0);
+        const bool used = C::CP > 0 ? ci < 2 * C::CP * (2 * C::RQ + 1) : in_support<C::SHAPE, C::RR, C::Q>(oz, oy, ox);
+        cf[ci] = used ? (C::PINC ? pin(p.coef[ci]) : p.coef[ci]) : T(0);
     }
     Consumer<C> cs;
     const T* __restrict__ src = p.src;
@@ -976,8 +1010,9 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
     prm.src = static_cast<const T*>(c.src);
     prm.dst = static_cast<T*>(c.dst);
     fill_geom(L, &prm.g);
-    if ((int)c.coef->size() != C::NC) return set_error(STENCIL_EUNSUPPORTED, "coefficient table size mismatch");
-    for (int i = 0; i < C::NC; ++i) prm.coef[i] = static_cast<T>((*c.coef)[i]);
+    if ((int)c.coef->size() > C::NC || (C::CP == 0 && (int)c.coef->size() != C::NC))
+        return set_error(STENCIL_EUNSUPPORTED, "coefficient table size mismatch");
+    for (int i = 0; i < (int)c.coef->size(); ++i) prm.coef[i] = static_cast<T>((*c.coef)[i]);
 
     std::vector<Box> boxes;
     for (const Box& b : c.boxes)

@@ -83,6 +83,6 @@ inline void fill_geom(const Layout3& L, DevGeom* g) {
     }
 }
 
-bool sweep_supported(const Plan* p, int q, int s);
+bool sweep_supported(const Plan* p, int q, int s, int rank = 0);
 
 }  // namespace sb

@@ -129,3 +129,54 @@ def test_periodic_layout_has_ghost_ring():
         assert tuple(p.frame_view(p.empty("cpu")).shape) == (40 + 2 * r, 30 + 2 * r)
     with pytest.raises(StencilError):
         Plan((64, 32), 1, "star", synth.weights(5, 1), boundary="periodic").layout_dist(0, 2, 2)
+
+
+# ------------------------------------------------------------ counterparts (NEXT-3)
+def test_counterparts_paper_example_rank_one():
+    """The paper's uniform 2D9P, m = 2: every column of Lambda is a
+    multiple of lambda^(1) = {1,2,3,2,1} (the counterparts lambda^(2) = 2 lambda^(1),
+    lambda^(3) = 3 lambda^(1)), i.e. Lambda has rank 1 and one counterpart suffices."""
+    from conftest import read_golden
+    golden = np.array([[float(x) for x in row] for row in read_golden("fold_2d9p_uniform_m2.txt")])
+    p = Plan((64, 64), 1, "box", [1.0] * 9)
+    rank, a, b = p.fold_rank(2)
+    assert rank == 1
+    lam1 = np.array([1.0, 2.0, 3.0, 2.0, 1.0])
+    # the counterpart's vertical and horizontal weights are both multiples of lambda^(1)
+    assert np.allclose(a[0] / a[0][2], lam1 / 3.0, rtol=0, atol=1e-15)
+    assert np.allclose(b[0] / b[0][2], lam1 / 3.0, rtol=0, atol=1e-15)
+    assert np.allclose(np.outer(a[0], b[0]), golden, rtol=0, atol=1e-13)
+    # the plan's profitability choice (GPU Eq.3): 2 W rank = 10 FMAs < |supp| = 25
+    assert p.variant(2) == (2, 1, 1)
+    assert p.variant(4) == (4, 1, 1)     # 18 < 81
+
+
+@pytest.mark.parametrize("m", [1, 2, 4])
+def test_counterparts_separable_and_full_rank(m):
+    rng = np.random.default_rng(7)
+    u, v = rng.uniform(0.5, 1.5, 3), rng.uniform(0.5, 1.5, 3)
+    w_sep = np.outer(u, v).ravel()                        # separable box weights
+    p = Plan((64, 64), 1, "box", w_sep)
+    rank, a, b = p.fold_rank(m)
+    assert rank == 1
+    lam = p.fold_coeffs(m)
+    assert np.max(np.abs(np.einsum("ki,kj->ij", a, b) - lam)) <= 1e-14 * np.max(np.abs(lam))
+    # rank 2: a sum of two separable kernels
+    u2, v2 = rng.uniform(0.5, 1.5, 3), rng.uniform(0.5, 1.5, 3)
+    w2 = (np.outer(u, v) + np.outer(u2, v2)).ravel()
+    r2, a2, b2 = Plan((64, 64), 1, "box", w2).fold_rank(m)
+    lam2 = Plan((64, 64), 1, "box", w2).fold_coeffs(m)
+    # (A + B)^{*m} = sum_i C(m,i) A^{*i} B^{*(m-i)}: m + 1 separable terms at most
+    assert r2 <= m + 1 and np.allclose(np.einsum("ki,kj->ij", a2, b2), lam2, rtol=0,
+                                                      atol=1e-13 * np.max(lam2))
+    # generic random weights: full rank, so the dense folded pass is kept
+    pr = Plan((64, 64), 1, "box", synth.weights(9, 1))
+    assert pr.fold_rank(m)[0] == 2 * m + 1
+    assert pr.variant(m)[2] == 0
+
+
+def test_counterparts_can_be_disabled():
+    p = Plan((64, 64), 1, "box", [1.0 / 9] * 9)
+    assert p.variant(2)[2] == 1
+    p.set_counterparts(False)
+    assert p.variant(2)[2] == 0

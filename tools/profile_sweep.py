@@ -19,7 +19,8 @@ a = ap.parse_args()
 cfg = CONFIGS[a.config]
 nd = len(cfg["dims"])
 k = {(1, "star"): 3, (2, "star"): 5, (2, "box"): 9, (3, "star"): 7, (3, "box"): 27}[(nd, cfg["shape"])]
-plan = Plan(cfg["dims"], 1, cfg["shape"], synth.weights(k, 1), cfg["dtype"])
+from bench import config_weights  # noqa: E402
+plan = Plan(cfg["dims"], 1, cfg["shape"], config_weights(cfg, k), cfg["dtype"])
 x, y, w = plan.empty(), plan.empty(), plan.empty()
 plan.fill_random(x, 2)
 plan.run(x, y, a.m * a.sweeps, a.m, w, a.stages)
