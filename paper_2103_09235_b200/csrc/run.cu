@@ -120,7 +120,10 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
         sc.coef = &folded(p, s.v.q);
     }
     sc.stream = stream;
-    if (s.m > 1) {
+    // STENCIL_DEBUG_NO_BAND=1 drops the band (WRONG results near FIXED faces):
+    // only to measure what the band costs (tools/, never in tests or bench)
+    static const bool no_band = getenv("STENCIL_DEBUG_NO_BAND") != nullptr;
+    if (s.m > 1 && !no_band) {
         for (const Box& b : band) {
             Box c = clip0(b, z0, z1);
             if (!c.empty()) sc.band.push_back(c);

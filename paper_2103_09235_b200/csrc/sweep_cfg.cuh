@@ -43,6 +43,9 @@ namespace sb {
 #ifndef SB_ROT_2D
 #define SB_ROT_2D 0
 #endif
+#ifndef SB_ROT_2DH
+#define SB_ROT_2DH 0
+#endif
 #ifndef SB_ROT_3D
 #define SB_ROT_3D 0
 #endif
@@ -79,7 +82,8 @@ template <typename T, int SHAPE, int Q, int S, int RR = 1>
 using Cfg2 = Cfg<T, 2, SHAPE, RR, Q, S, (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NTXH : SB_2D_NTX), 1, 1,
                  (plc2<Q, RR>() ? 0 : SB_2D_PB),
                  (plc2<Q, RR>() ? SB_2D_NSLOT_PLC : vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NSLOTH : SB_2D_NSLOT),
-                 vxm2<SHAPE, Q, RR>(), (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_MINBH : SB_2D_MINB), SB_ROT_2D, SB_PINC_2D>;
+                 vxm2<SHAPE, Q, RR>(), (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_MINBH : SB_2D_MINB),
+                 (vxm2<SHAPE, Q, RR>() > 1 && !plc2<Q, RR>() ? SB_ROT_2DH : SB_ROT_2D), SB_PINC_2D>;
 // The folded 3D star pass with Q = 2 (25 taps, C4 m=2) takes 4 output rows per
 // thread (more FMAs per shared-memory row), 2-plane slots and pinned
 // coefficients (measured 514 vs 458 GStencil/s); the rest use the defaults.

@@ -318,11 +318,16 @@ __device__ __forceinline__ void band_block(const BandDesc<typename C::T>& bd, co
         const bool rowin = a0 >= 0 && a0 < g.ext[0] && a1 >= 0 && a1 < g.ext[1];
         const T* gp = src + a0 * s0 + a1 * s1 + g.origin[2] + ilo[2];
         T* sp = cur + c0 * S0 + c1 * S1;
+        // cp.async (LDGSTS): global -> shared without a register round trip, so
+        // every thread keeps many loads in flight (the band is latency-bound);
+        // cells outside the allocation are zero-filled (src-size 0).
         for (int c2 = lx; c2 < ie[2]; c2 += LX) {
             const long long a2 = g.origin[2] + ilo[2] + c2;
-            sp[c2] = (rowin && a2 >= 0 && a2 < g.ext[2]) ? gp[c2] : T(0);
+            const bool ok = rowin && a2 >= 0 && a2 < g.ext[2];
+            ptx::cp_async<sizeof(T)>(sp + c2, ok ? gp + c2 : src, ok);
         }
     });
+    ptx::cp_async_wait_all();
     __syncthreads();
     for (int s = 1; s <= bd.m; ++s) {
         int rlo[3], re[3];
