@@ -231,7 +231,7 @@ def run_ours(args):
 
     import synth
     from paper_2103_09235_b200 import Plan
-    from paper_2103_09235_b200.dist import make_comm
+    from paper_2103_09235_b200.dist import make_comm, make_peer_comm
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
@@ -258,7 +258,8 @@ def run_ours(args):
         L = plan.layout_dist(rank, world, halo)
         a, b, ws = (plan.empty(layout=L) for _ in range(3))
         plan.fill_random_dist(rank, world, halo, a, synth.DEFAULT_SEED_U)
-        comm = make_comm(dev)
+        # NCCL send/recv per sweep (default), or the fused peer stores of NEXT-2
+        comm = make_peer_comm(b, ws, dev) if args.exchange == "peer" else make_comm(dev)
     else:
         L = plan.layout
         a, b, ws = plan.empty(), plan.empty(), plan.empty()
@@ -441,6 +442,7 @@ def run_ours(args):
                               "L2 flushed before every step (256 MB write, outside the step's events): "
                               "buffers are %.1f MB" % (L.bytes / 1e6)),
                        "parallelism": "slab%d" % world if world > 1 else "single",
+                       "exchange": args.exchange if world > 1 else None,
                        "cuda_graph": use_graph,
                        "evaluation": dict(zip(("q", "stages", "counterparts"), plan.variant(m)))
                        if args.stages == 0 and nd >= 2 else {"stages": args.stages or "auto"}},
@@ -469,6 +471,8 @@ def main():
                     help="default: the config's measured-best fold_m; 0 = measure every fold_m of the config")
     ap.add_argument("--stages", type=int, default=0, help="0 = the plan's choice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
+                    help="N>1 halo exchange: NCCL send/recv (default) or fused peer stores (NEXT-2)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

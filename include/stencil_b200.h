@@ -266,14 +266,38 @@ int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void *buf, int h
                           void *stream);
 
 /*
+ * Fused halo exchange over peer memory (one process per
+ * GPU, NVLink/NVSwitch peers).  Instead of an NCCL kernel per sweep, the sweep
+ * kernel stores the outputs of its first/last fold_m*r planes a second time,
+ * straight into the neighbours' ghost planes (CUDA IPC peer pointers), so the
+ * transfer overlaps the math tile by tile; GPUs order their sweeps with
+ * stream memory operations on small flag words (cuStreamWriteValue32 after
+ * each sweep, cuStreamWaitValue32 before the next: no spinning kernel).
+ *   1. stencil_comm_create_peer(&c, rank, nranks, buf0, buf1): buf0/buf1 =
+ *      this rank's ping-pong buffers (every run must pass them as out and
+ *      workspace, in either order);
+ *   2. stencil_comm_peer_handles(c, rec): writes 3 * STENCIL_PEER_HANDLE_BYTES;
+ *   3. all-gather the records (rank order) and stencil_comm_peer_attach(c, all);
+ *   4. stencil_run_dist(plan, c, ...) as with an NCCL comm.
+ * Errors: EINVAL (NULL, bad rank, buffers not the registered pair), ECUDA
+ * (IPC / stream memory operations unavailable or failing).
+ */
+#define STENCIL_PEER_HANDLE_BYTES 72
+int stencil_comm_create_peer(stencil_comm *comm, int rank, int nranks, void *buf0, void *buf1);
+int stencil_comm_peer_handles(stencil_comm comm, unsigned char *out);
+int stencil_comm_peer_attach(stencil_comm comm, const unsigned char *all);
+
+/*
  * The same distributed algorithm with all `nranks` ranks in THIS process on
- * the current device, exchanging ghost planes with device-to-device copies
- * instead of NCCL (identical kernels, boxes and ordering; used by tests on
- * one GPU).  Arrays of nranks pointers.
+ * the current device (identical kernels, boxes and ordering; used by tests on
+ * one GPU).  exchange = 0: the NCCL path's schedule, its transport done with
+ * device-to-device copies; exchange = 1: the fused peer-store path (the
+ * neighbours' buffers are plain device pointers here).  Arrays of nranks
+ * pointers.
  */
 int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void *const *in_locals,
                               void *const *out_locals, int64_t T, int fold_m, int stages,
-                              int halo, void *const *workspaces, void *stream);
+                              int halo, void *const *workspaces, int exchange, void *stream);
 
 /* Thread-local message for the last error on this thread ("" if none). */
 const char *stencil_last_error(void);

@@ -54,7 +54,10 @@ SIGNATURES = {
     "stencil_run_dist": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_int, c_vp, c_vp]),
     "stencil_halo_exchange": (c_int, [c_vp, c_vp, c_vp, c_int, c_vp]),
     "stencil_run_dist_emulated": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i64, c_int,
-                                          c_int, c_int, ctypes.POINTER(c_vp), c_vp]),
+                                          c_int, c_int, ctypes.POINTER(c_vp), c_int, c_vp]),
+    "stencil_comm_create_peer": (c_int, [ctypes.POINTER(c_vp), c_int, c_int, c_vp, c_vp]),
+    "stencil_comm_peer_handles": (c_int, [c_vp, ctypes.c_char_p]),
+    "stencil_comm_peer_attach": (c_int, [c_vp, ctypes.c_char_p]),
     "stencil_last_error": (ctypes.c_char_p, []),
     "stencil_version": (ctypes.c_char_p, []),
 }

@@ -220,13 +220,17 @@ class Plan:
     def halo_exchange(self, comm: "Comm", buf, halo, stream=None):
         check(self._lib.stencil_halo_exchange(self._h, comm._h, _ptr(buf), int(halo), _stream(stream)))
 
-    def run_dist_emulated(self, ins, outs, T, fold_m, halo, workspaces=None, stages=0, stream=None):
+    def run_dist_emulated(self, ins, outs, T, fold_m, halo, workspaces=None, stages=0, stream=None,
+                          exchange="copies"):
+        """All ranks in this process on one GPU; exchange = "copies" (the NCCL
+        path's schedule with device-to-device copies) or "peer" (fused peer stores)."""
         n = len(ins)
         arr = ctypes.c_void_p * n
         wp = arr(*[_ptr(w) for w in workspaces]) if workspaces is not None else None
+        mode = {"copies": 0, "peer": 1}[exchange]
         check(self._lib.stencil_run_dist_emulated(self._h, n, arr(*[_ptr(t) for t in ins]),
                                                   arr(*[_ptr(t) for t in outs]), int(T), int(fold_m), int(stages),
-                                                  int(halo), wp, _stream(stream)))
+                                                  int(halo), wp, mode, _stream(stream)))
 
 
 class Comm:
@@ -247,6 +251,34 @@ class Comm:
         buf = ctypes.create_string_buffer(128)
         check(load().stencil_comm_unique_id(buf))
         return buf.raw
+
+    @classmethod
+    def peer(cls, rank: int, nranks: int, buf0, buf1) -> "Comm":
+        """Fused peer-store exchange (NEXT-2): buf0/buf1 are this rank's
+        ping-pong buffers (every run passes them as out and workspace).  Attach
+        the neighbours with attach(all_records) after an all-gather of
+        handles() (paper_2103_09235_b200.dist.make_peer_comm does both)."""
+        self = cls.__new__(cls)
+        self._lib = load()
+        h = ctypes.c_void_p()
+        check(self._lib.stencil_comm_create_peer(ctypes.byref(h), int(rank), int(nranks), _ptr(buf0), _ptr(buf1)))
+        self._h = h
+        self.rank, self.nranks = rank, nranks
+        return self
+
+    PEER_RECORD = 3 * 72   # 3 x STENCIL_PEER_HANDLE_BYTES
+
+    def handles(self) -> bytes:
+        buf = ctypes.create_string_buffer(self.PEER_RECORD)
+        check(self._lib.stencil_comm_peer_handles(self._h, buf))
+        return buf.raw
+
+    def attach(self, records) -> None:
+        """records: every rank's handles() in rank order."""
+        blob = b"".join(records)
+        if len(blob) != self.PEER_RECORD * self.nranks:
+            raise ValueError("expected %d records of %d bytes" % (self.nranks, self.PEER_RECORD))
+        check(self._lib.stencil_comm_peer_attach(self._h, blob))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -220,13 +220,17 @@ int launch_1d(Plan* p, const void* src, void* dst, const Layout3* L, int64_t TB,
 // Copy every non-interior cell (frozen ring, ghost planes, pads) src -> dst,
 // one warp per row of the allocation.
 template <typename T>
-__global__ void ring_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, DevGeom g, long long rows) {
+__global__ void ring_copy_kernel(const T* __restrict__ src, T* __restrict__ dst, DevGeom g, long long rows,
+                                 int keep_ghost_interior) {
     long long row = (long long)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     if (row >= rows) return;
     const int lane = threadIdx.x & 31;
     long long r0 = row / g.ext[1], r1 = row % g.ext[1];
     long long c0 = r0 - g.origin[0], c1 = r1 - g.origin[1];
-    bool inside = c0 >= 0 && c0 < g.n[0] && c1 >= 0 && c1 < g.n[1];
+    // a ghost plane (non-physical face) counts as interior along axis 0 when its
+    // interior cells are owned by the neighbours' stores
+    const bool ghost0 = keep_ghost_interior && ((c0 < 0 && !g.phys_lo[0]) || (c0 >= g.n[0] && !g.phys_hi[0]));
+    bool inside = (ghost0 || (c0 >= 0 && c0 < g.n[0])) && c1 >= 0 && c1 < g.n[1];
     long long base = r0 * g.stride0 + r1 * g.stride1;
     if (!inside) {
         for (long long x = lane; x < g.ext[2]; x += 32) dst[base + x] = src[base + x];
@@ -237,7 +241,7 @@ __global__ void ring_copy_kernel(const T* __restrict__ src, T* __restrict__ dst,
     }
 }
 
-int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void* stream) {
+int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void* stream, bool keep_ghost_interior) {
     DevGeom g;
     fill_geom(*L, &g);
     long long rows = L->ext[0] * L->ext[1];
@@ -245,10 +249,10 @@ int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void
     unsigned blocks = (unsigned)((rows + wpb - 1) / wpb);
     if (p->dtype == STENCIL_F64)
         ring_copy_kernel<double><<<blocks, wpb * 32, 0, (cudaStream_t)stream>>>(
-            static_cast<const double*>(src), static_cast<double*>(dst), g, rows);
+            static_cast<const double*>(src), static_cast<double*>(dst), g, rows, keep_ghost_interior ? 1 : 0);
     else
         ring_copy_kernel<float><<<blocks, wpb * 32, 0, (cudaStream_t)stream>>>(
-            static_cast<const float*>(src), static_cast<float*>(dst), g, rows);
+            static_cast<const float*>(src), static_cast<float*>(dst), g, rows, keep_ghost_interior ? 1 : 0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "ring_copy_kernel launch");
     return 1;

@@ -103,6 +103,10 @@ struct SweepCall {
     int q, stages;
     const std::vector<double>* coef;   // lambda^(q), dense fp64 (or packed a_k | b_k when rank > 0)
     int rank = 0;                      // counterpart evaluation (Variant::rank)
+    // fused halo exchange (NEXT-2): neighbour buffers of the same parity as dst
+    void* peer_lo = nullptr;           // rank - 1 (receives local planes [0, peer_h))
+    void* peer_hi = nullptr;           // rank + 1 (receives local planes [n0 - peer_h, n0))
+    int peer_h = 0;
     std::vector<Box> band;    // exact stepwise band boxes (K-G3), same launch
     int band_m = 1;           // steps of the band (the sweep's fold_m)
     void* stream;
@@ -117,7 +121,10 @@ int onchip1d_cells_per_lane(int r, int m, bool wrap);   // V of the warp window 
 // PERIODIC: fill every ghost cell of buf from its wrapped interior cell.
 int launch_wrap_fill(Plan* p, void* buf, const Layout3* L, void* stream);
 // Copy every non-interior cell (ring, ghosts, pads) src -> dst (K-G5).
-int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void* stream);
+// keep_ghost_interior: leave the interior (y, x) cells of non-physical ghost
+// planes alone (the fused exchange's neighbours write them).
+int launch_ring_copy(Plan* p, const void* src, void* dst, const Layout3* L, void* stream,
+                     bool keep_ghost_interior = false);
 // K-G0 seeded field over the frame (global padded index).
 int launch_fill(Plan* p, void* buf, const Layout3* L, uint64_t seed, void* stream);
 

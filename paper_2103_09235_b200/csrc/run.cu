@@ -3,6 +3,7 @@
 // (P:410), the main-region sweep plus the exact boundary band per sweep, and
 // the slab-decomposed multi-GPU run with a per-sweep halo exchange
 // (NCCL send/recv on a comm stream, overlapped with the interior).
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
@@ -96,7 +97,8 @@ struct SweepSpec {
 
 // Enqueue one sweep restricted to axis-0 range [z0, z1). Returns launches or <0.
 static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, const SweepSpec& s,
-                         int64_t z0, int64_t z1, void* stream) {
+                         int64_t z0, int64_t z1, void* stream, void* peer_lo = nullptr, void* peer_hi = nullptr,
+                         int peer_h = 0) {
     Box mainb;
     std::vector<Box> band;
     split_band(L, s.m, &mainb, &band);
@@ -110,6 +112,9 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
     sc.q = s.v.q;
     sc.stages = s.v.stages;
     sc.rank = s.v.rank;
+    sc.peer_lo = peer_lo;
+    sc.peer_hi = peer_hi;
+    sc.peer_h = (peer_lo || peer_hi) ? peer_h : 0;
     std::vector<double> packed;
     if (s.v.rank > 0) {   // counterparts: a_0..a_{rank-1} | b_0..b_{rank-1}
         const LowRank& lr = lowrank(p, s.v.q);
@@ -346,6 +351,32 @@ static int nccl_error(ncclResult_t r, const char* what) {
     return set_error(STENCIL_ENCCL, std::string(what) + ": " + (a.GetErrorString ? a.GetErrorString(r) : "?"));
 }
 
+// Stream memory operations and address-range query (driver API, resolved at
+// run time like the TMA encoder): the fused exchange's inter-GPU sweep flags.
+struct DrvMemOps {
+    CUresult (*wait32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+    CUresult (*write32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int) = nullptr;
+    CUresult (*range)(CUdeviceptr*, size_t*, CUdeviceptr) = nullptr;
+};
+static DrvMemOps& drv() {
+    static DrvMemOps d;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            d.wait32 = reinterpret_cast<decltype(d.wait32)>(f);
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            d.write32 = reinterpret_cast<decltype(d.write32)>(f);
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            d.range = reinterpret_cast<decltype(d.range)>(f);
+    });
+    return d;
+}
+
 }  // namespace sb
 
 struct stencil_comm_s {
@@ -353,6 +384,16 @@ struct stencil_comm_s {
     int rank = 0, nranks = 1;
     cudaStream_t cstream = nullptr;
     cudaEvent_t evA = nullptr, evC = nullptr;
+    // fused peer-store exchange (NEXT-2): this rank's two ping-pong buffers, the
+    // neighbours' buffers mapped through CUDA IPC, and sweep flags: flags[0] is
+    // written by rank - 1, flags[1] by rank + 1 (stream memory operations).
+    bool peer = false;
+    void* buf[2] = {nullptr, nullptr};
+    void* nbuf[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};   // [side 0 = lo, 1 = hi][buffer]
+    void* nbase[2][3] = {{nullptr, nullptr, nullptr}, {nullptr, nullptr, nullptr}};   // opened IPC bases
+    uint32_t* flags = nullptr;
+    uint32_t* nflag[2] = {nullptr, nullptr};   // neighbour's flag slot this rank writes
+    uint32_t epoch = 0;
 };
 
 namespace sb {
@@ -406,6 +447,75 @@ static int sweep_phase(Plan* p, const Layout3& L, const void* src, void* dst, co
 static size_t plane_bytes(const Layout3& L) { return (size_t)L.stride[0] * L.esize; }
 
 }  // namespace sb
+
+// ------------------------------------------------------------------ fused exchange (NEXT-2)
+// One launch per sweep over the whole slab: the sweep kernel stores the
+// outputs of its first/last hx planes a second time, straight into the
+// neighbours' ghost planes of the same ping-pong parity (CUDA IPC peer
+// pointers over NVLink), so the transfer overlaps the math tile by tile and
+// there is no NCCL kernel.  Ordering between GPUs: after sweep j a rank writes
+// the sweep counter into each neighbour's flag (cuStreamWriteValue32, which
+// fences the kernel's stores first); before sweep j+1 it waits until both
+// neighbours' counters reached j (cuStreamWaitValue32, a stream-level wait, no
+// spinning kernel).  That covers both hazards: the ghosts read by sweep j+1
+// were written by the neighbours' sweep j, and a neighbour's sweep j+1 writes
+// into the buffer this rank read during sweep j.
+static int run_dist_peer(sb::Plan* p, stencil_comm_s* c, const sb::Layout3& L, const void* in_local, void* out_local,
+                         void* ws, int64_t n, int64_t nf, int fold_m, sb::Variant v, int64_t hx, void* stream) {
+    using namespace sb;
+    if (!((out_local == c->buf[0] && (n < 2 || ws == c->buf[1])) ||
+          (out_local == c->buf[1] && (n < 2 || ws == c->buf[0]))))
+        return set_error(STENCIL_EINVAL, "peer comm: out/workspace must be the buffers the comm was created with");
+    const int bo = out_local == c->buf[0] ? 0 : 1;   // registered index of `out`
+    DrvMemOps& d = drv();
+    if (!d.wait32 || !d.write32) return set_error(STENCIL_ECUDA, "cuStreamWaitValue32/WriteValue32 unavailable");
+    CUstream cs = (CUstream)stream;
+    int launches = 0;
+    // ring/pads only: the interior cells of the ghost planes belong to the
+    // neighbours' peer stores (they may already be writing them)
+    int rc = launch_ring_copy(p, in_local, out_local, &L, stream, true);
+    if (rc < 0) return rc;
+    launches += rc;
+    if (n >= 2) {
+        rc = launch_ring_copy(p, in_local, ws, &L, stream, true);
+        if (rc < 0) return rc;
+        launches += rc;
+    }
+    const bool has_lo = c->rank > 0, has_hi = c->rank < c->nranks - 1;
+    void* bufs[2] = {out_local, ws};
+    for (int64_t j = 1; j <= n; ++j) {
+        SweepSpec s;
+        s.m = j <= nf ? fold_m : 1;
+        s.v = j <= nf ? v : Variant{1, 1};
+        const void* src = j == 1 ? in_local : bufs[(n - j + 1) % 2];
+        const int di = (int)((n - j) % 2);           // 0 = out, 1 = ws
+        const int reg = di == 0 ? bo : 1 - bo;       // registered index of dst
+        {   // the neighbours finished sweep j-1 (for j = 1: their previous run)
+            const uint32_t want = c->epoch + (uint32_t)(j - 1);
+            if (has_lo && d.wait32(cs, (CUdeviceptr)(c->flags + 0), want, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return set_error(STENCIL_ECUDA, "cuStreamWaitValue32");
+            if (has_hi && d.wait32(cs, (CUdeviceptr)(c->flags + 1), want, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+                return set_error(STENCIL_ECUDA, "cuStreamWaitValue32");
+        }
+        const bool xchg = j < n;
+        rc = enqueue_sweep(p, L, src, bufs[di], s, 0, L.n[0], stream, xchg && has_lo ? c->nbuf[0][reg] : nullptr,
+                           xchg && has_hi ? c->nbuf[1][reg] : nullptr, (int)hx);
+        if (rc < 0) return rc;
+        launches += rc;
+        {   // every sweep signals, the last one included (orders the next run)
+            const uint32_t val = c->epoch + (uint32_t)j;
+            if (has_lo && d.write32(cs, (CUdeviceptr)c->nflag[0], val, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+                return set_error(STENCIL_ECUDA, "cuStreamWriteValue32");
+            if (has_hi && d.write32(cs, (CUdeviceptr)c->nflag[1], val, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+                return set_error(STENCIL_ECUDA, "cuStreamWriteValue32");
+        }
+    }
+    c->epoch += (uint32_t)n;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "run_dist_peer");
+    p->last_launches = launches;
+    return STENCIL_OK;
+}
 
 using namespace sb;
 
@@ -544,8 +654,85 @@ int stencil_comm_create(stencil_comm* comm, const unsigned char id[128], int ran
     return STENCIL_OK;
 }
 
+// ---- fused peer-store exchange (NEXT-2)
+int stencil_comm_create_peer(stencil_comm* comm, int rank, int nranks, void* buf0, void* buf1) {
+    if (!comm || !buf0 || !buf1) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (nranks < 1 || rank < 0 || rank >= nranks) return set_error(STENCIL_EINVAL, "bad rank/nranks");
+    if (buf0 == buf1) return set_error(STENCIL_EINVAL, "the two buffers must differ");
+    *comm = nullptr;
+    stencil_comm_s* c = new stencil_comm_s();
+    c->rank = rank;
+    c->nranks = nranks;
+    c->peer = true;
+    c->buf[0] = buf0;
+    c->buf[1] = buf1;
+    cudaError_t e = cudaMalloc(&c->flags, 256);   // own allocation: exported alone
+    if (e == cudaSuccess) e = cudaMemset(c->flags, 0, 256);
+    if (e != cudaSuccess) {
+        delete c;
+        return cuda_error(e, "flags");
+    }
+    *comm = c;
+    return STENCIL_OK;
+}
+
+// 3 records of STENCIL_PEER_HANDLE_BYTES (buf0, buf1, flags): a 64-byte CUDA
+// IPC handle of the allocation holding the pointer + the 8-byte offset into it.
+int stencil_comm_peer_handles(stencil_comm comm, unsigned char* out) {
+    if (!comm || !out) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (!comm->peer) return set_error(STENCIL_EINVAL, "not a peer comm");
+    DrvMemOps& d = drv();
+    if (!d.range) return set_error(STENCIL_ECUDA, "cuMemGetAddressRange unavailable");
+    void* ptrs[3] = {comm->buf[0], comm->buf[1], comm->flags};
+    for (int i = 0; i < 3; ++i) {
+        CUdeviceptr base = 0;
+        size_t size = 0;
+        if (d.range(&base, &size, (CUdeviceptr)ptrs[i]) != CUDA_SUCCESS)
+            return set_error(STENCIL_ECUDA, "cuMemGetAddressRange");
+        cudaIpcMemHandle_t h;
+        cudaError_t e = cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base));
+        if (e != cudaSuccess) return cuda_error(e, "cudaIpcGetMemHandle");
+        uint64_t off = (uint64_t)((CUdeviceptr)ptrs[i] - base);
+        std::memcpy(out + i * STENCIL_PEER_HANDLE_BYTES, &h, 64);
+        std::memcpy(out + i * STENCIL_PEER_HANDLE_BYTES + 64, &off, 8);
+    }
+    return STENCIL_OK;
+}
+
+// all: nranks x 3 records, in rank order (what every rank's peer_handles wrote).
+int stencil_comm_peer_attach(stencil_comm comm, const unsigned char* all) {
+    if (!comm || !all) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (!comm->peer) return set_error(STENCIL_EINVAL, "not a peer comm");
+    const int nb[2] = {comm->rank - 1, comm->rank + 1};
+    for (int side = 0; side < 2; ++side) {
+        const int g = nb[side];
+        if (g < 0 || g >= comm->nranks) continue;
+        for (int i = 0; i < 3; ++i) {
+            const unsigned char* rec = all + ((size_t)g * 3 + i) * STENCIL_PEER_HANDLE_BYTES;
+            cudaIpcMemHandle_t h;
+            uint64_t off = 0;
+            std::memcpy(&h, rec, 64);
+            std::memcpy(&off, rec + 64, 8);
+            void* base = nullptr;
+            cudaError_t e = cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess) return cuda_error(e, "cudaIpcOpenMemHandle");
+            comm->nbase[side][i] = base;
+            char* ptr = static_cast<char*>(base) + off;
+            if (i < 2) comm->nbuf[side][i] = ptr;
+            // the neighbour's flag this rank writes: the lower neighbour hears from
+            // its upper side (slot 1), the upper neighbour from its lower side (slot 0)
+            else comm->nflag[side] = reinterpret_cast<uint32_t*>(ptr) + (side == 0 ? 1 : 0);
+        }
+    }
+    return STENCIL_OK;
+}
+
 int stencil_comm_destroy(stencil_comm comm) {
     if (!comm) return STENCIL_OK;
+    for (auto& side : comm->nbase)
+        for (void*& b : side)
+            if (b) cudaIpcCloseMemHandle(b);
+    if (comm->flags) cudaFree(comm->flags);
     NcclApi& a = nccl();
     if (comm->comm && a.ok) a.CommDestroy(comm->comm);
     if (comm->evA) cudaEventDestroy(comm->evA);
@@ -609,6 +796,7 @@ int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local,
     const int64_t nf = T / fold_m, nr = T % fold_m, n = nf + nr;
     if (n >= 2 && !workspace) return set_error(STENCIL_EINVAL, "workspace required");
     const int64_t hx = (int64_t)fold_m * p->r;
+    if (comm->peer) return run_dist_peer(p, comm, L, in_local, out_local, workspace, n, nf, fold_m, v, hx, stream);
     int launches = 0;
     rc = launch_ring_copy(p, in_local, out_local, &L, stream);
     if (rc < 0) return rc;
@@ -648,7 +836,8 @@ int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local,
 }
 
 int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void* const* in_locals, void* const* out_locals,
-                              int64_t T, int fold_m, int stages, int halo, void* const* workspaces, void* stream) {
+                              int64_t T, int fold_m, int stages, int halo, void* const* workspaces, int exchange,
+                              void* stream) {
     Plan* p = reinterpret_cast<Plan*>(plan);
     if (!p || !in_locals || !out_locals || nranks < 1) return set_error(STENCIL_EINVAL, "bad argument");
     std::vector<Layout3> Ls(nranks);
@@ -683,6 +872,36 @@ int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void* const* 
             rc = launch_ring_copy(p, in_locals[g], workspaces[g], &Ls[g], stream);
             if (rc < 0) return rc;
         }
+    }
+    if (exchange == 1) {
+        // fused peer stores (NEXT-2): one launch per rank and sweep over the whole
+        // slab; the kernel itself stores its boundary planes into the
+        // neighbours' ghost planes (here plain device pointers on this GPU; the
+        // ranks run one after another on one stream, so no flags are needed)
+        for (int64_t j = 1; j <= n; ++j) {
+            SweepSpec s;
+            s.m = j <= nf ? fold_m : 1;
+            s.v = j <= nf ? v : Variant{1, 1};
+            std::vector<void*> dsts(nranks);
+            for (int g = 0; g < nranks; ++g) {
+                void* bufs[2] = {out_locals[g], workspaces ? workspaces[g] : nullptr};
+                dsts[g] = bufs[(n - j) % 2];
+            }
+            for (int g = 0; g < nranks; ++g) {
+                void* bufs[2] = {out_locals[g], workspaces ? workspaces[g] : nullptr};
+                const void* src = j == 1 ? in_locals[g] : bufs[(n - j + 1) % 2];
+                const bool xchg = j < n;
+                rc = enqueue_sweep(p, Ls[g], src, dsts[g], s, 0, Ls[g].n[0], stream,
+                                   xchg && g > 0 ? dsts[g - 1] : nullptr,
+                                   xchg && g < nranks - 1 ? dsts[g + 1] : nullptr, (int)hx);
+                if (rc < 0) return rc;
+                launches += rc;
+            }
+        }
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return cuda_error(e, "run_dist_emulated");
+        p->last_launches = launches;
+        return STENCIL_OK;
     }
     for (int64_t j = 1; j <= n; ++j) {
         SweepSpec s;

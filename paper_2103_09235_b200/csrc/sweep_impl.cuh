@@ -280,10 +280,15 @@ __device__ __forceinline__ void band_rows(int n0, int n1, int n2, int tid, int n
     }
 }
 
+struct PeerStores {
+    long long dlo, dhi;   // byte deltas to the neighbours' ghost planes
+    int h, lo_on, hi_on;
+};
+
 template <class C>
 __device__ __forceinline__ void band_block(const BandDesc<typename C::T>& bd, const DevGeom& g,
                                            const typename C::T* __restrict__ src, typename C::T* __restrict__ dst,
-                                           int blk_id, typename C::T* smem, int tid, int nthr) {
+                                           int blk_id, typename C::T* smem, int tid, int nthr, const PeerStores& ps) {
     using T = typename C::T;
     constexpr int RR = C::RR;
     constexpr bool used[3] = {true, C::ND == 3, true};
@@ -376,6 +381,17 @@ __device__ __forceinline__ void band_block(const BandDesc<typename C::T>& bd, co
         const T* sp = cur + (olo[0] - ilo[0] + d0) * S0 + (olo[1] - ilo[1] + d1) * S1 + (olo[2] - ilo[2]);
         T* gp = dst + (g.origin[0] + olo[0] + d0) * s0 + (g.origin[1] + olo[1] + d1) * s1 + g.origin[2] + olo[2];
         for (int d2 = lx; d2 < oe2; d2 += LX) gp[d2] = sp[d2];
+        if (ps.h > 0) {   // fused halo exchange (NEXT-2)
+            const int z = olo[0] + d0;
+            if (ps.lo_on && z < ps.h) {
+                T* q = reinterpret_cast<T*>(reinterpret_cast<char*>(gp) + ps.dlo);
+                for (int d2 = lx; d2 < oe2; d2 += LX) q[d2] = sp[d2];
+            }
+            if (ps.hi_on && z >= g.n[0] - ps.h) {
+                T* q = reinterpret_cast<T*>(reinterpret_cast<char*>(gp) + ps.dhi);
+                for (int d2 = lx; d2 < oe2; d2 += LX) q[d2] = sp[d2];
+            }
+        }
     });
     __syncthreads();
 }
@@ -794,22 +810,32 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                 constexpr int dn = pmod(PH - C::H, C::NW);
                 const int z = z_in - C::H;
                 if (z >= out_lo && z < out_hi) {
+                    auto emit = [&](T* ob) {
 #pragma unroll
-                    for (int vy = 0; vy < C::VY; ++vy) {
-                        if (!(ymask & (1u << vy))) continue;
-                        T* op = optr + vy * s1;
+                        for (int vy = 0; vy < C::VY; ++vy) {
+                            if (!(ymask & (1u << vy))) continue;
+                            T* op = ob + vy * s1;
 #pragma unroll
-                        for (int mm = 0; mm < C::VX / C::VEC; ++mm) {
-                            if (vmask & (1u << mm)) {
-                                VecT<T>::st(op + mm * C::VEC, &cs.acc[C::S - 1][dn][vy][mm * C::VEC]);
-                            } else {
+                            for (int mm = 0; mm < C::VX / C::VEC; ++mm) {
+                                if (vmask & (1u << mm)) {
+                                    VecT<T>::st(op + mm * C::VEC, &cs.acc[C::S - 1][dn][vy][mm * C::VEC]);
+                                } else {
 #pragma unroll
-                                for (int e = 0; e < C::VEC; ++e) {
-                                    const int x = gx + mm * C::VEC + e;
-                                    if (x >= xlo && x < xhi) op[mm * C::VEC + e] = cs.acc[C::S - 1][dn][vy][mm * C::VEC + e];
+                                    for (int e = 0; e < C::VEC; ++e) {
+                                        const int x = gx + mm * C::VEC + e;
+                                        if (x >= xlo && x < xhi)
+                                            op[mm * C::VEC + e] = cs.acc[C::S - 1][dn][vy][mm * C::VEC + e];
+                                    }
                                 }
                             }
                         }
+                    };
+                    emit(optr);
+                    if (p.peer_h > 0) {   // fused halo exchange: the neighbours' ghost planes, over NVLink
+                        if (p.peer_lo_on && z < p.peer_h)
+                            emit(reinterpret_cast<T*>(reinterpret_cast<char*>(optr) + p.peer_dlo));
+                        if (p.peer_hi_on && z >= p.g.n[0] - p.peer_h)
+                            emit(reinterpret_cast<T*>(reinterpret_cast<char*>(optr) + p.peer_dhi));
                     }
                 }
                 optr += s0;
@@ -875,7 +901,8 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             __syncthreads();
             const int blk = s_blk;
             if (blk >= p.band.nblk_total) break;
-            band_block<C>(p.band, p.g, p.src, p.dst, blk, slots, threadIdx.x, C::NTHREADS);
+            band_block<C>(p.band, p.g, p.src, p.dst, blk, slots, threadIdx.x, C::NTHREADS,
+                          PeerStores{p.peer_dlo, p.peer_dhi, p.peer_h, p.peer_lo_on, p.peer_hi_on});
         }
     }
 }
@@ -1014,6 +1041,16 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
     std::memset(&prm, 0, sizeof(prm));
     prm.src = static_cast<const T*>(c.src);
     prm.dst = static_cast<T*>(c.dst);
+    if (c.peer_h > 0) {
+        const long long plane = (long long)L.n[0] * L.stride[0] * (long long)sizeof(T);
+        prm.peer_h = c.peer_h;
+        prm.peer_lo_on = c.peer_lo != nullptr;
+        prm.peer_hi_on = c.peer_hi != nullptr;
+        if (c.peer_lo)
+            prm.peer_dlo = (long long)(reinterpret_cast<intptr_t>(c.peer_lo) - reinterpret_cast<intptr_t>(c.dst)) + plane;
+        if (c.peer_hi)
+            prm.peer_dhi = (long long)(reinterpret_cast<intptr_t>(c.peer_hi) - reinterpret_cast<intptr_t>(c.dst)) - plane;
+    }
     fill_geom(L, &prm.g);
     if ((int)c.coef->size() > C::NC || (C::CP == 0 && (int)c.coef->size() != C::NC))
         return set_error(STENCIL_EUNSUPPORTED, "coefficient table size mismatch");

@@ -66,6 +66,12 @@ struct SweepParams {
     DevBoxes b;
     DevSched sc;
     BandDesc<T> band;
+    // Fused halo exchange (NEXT-2): outputs of local planes z < peer_h are also
+    // stored into the lower neighbour's ghost planes and those of z >= n0 - peer_h
+    // into the upper neighbour's, at the same element offset plus these byte
+    // deltas (neighbour buffer - dst +/- n0 planes); 0 = no such neighbour.
+    long long peer_dlo, peer_dhi;
+    int peer_h, peer_lo_on, peer_hi_on;
     T coef[NC];
 };
 

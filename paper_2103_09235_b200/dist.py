@@ -3,7 +3,8 @@
 Only bootstrap and host-side bookkeeping live here: the NCCL unique id is
 broadcast through the default process group (gloo or nccl), and the slab
 arithmetic mirrors stencil_plan_layout_dist.  The halo exchange itself runs
-inside the library (ncclSend/ncclRecv on its comm stream).
+inside the library (ncclSend/ncclRecv on its comm stream, or the fused
+peer stores of the sweep kernel with make_peer_comm).
 """
 from __future__ import annotations
 
@@ -22,6 +23,26 @@ def make_comm(device=None) -> Comm:
         t = t.to(device or torch.device("cuda", torch.cuda.current_device()))
     dist.broadcast(t, src=0)
     return Comm(bytes(t.cpu().tolist()), rank, world)
+
+
+def all_gather_bytes(blob: bytes, device=None):
+    """Every rank's `blob` (equal lengths) in rank order, over the default group."""
+    t = torch.tensor(list(blob), dtype=torch.uint8)
+    if dist.get_backend() == "nccl":
+        t = t.to(device or torch.device("cuda", torch.cuda.current_device()))
+    out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
+    dist.all_gather(out, t)
+    return [bytes(o.cpu().tolist()) for o in out]
+
+
+def make_peer_comm(buf0, buf1, device=None) -> Comm:
+    """The fused peer-store exchange (NEXT-2) over the current process group:
+    CUDA IPC handles of every rank's two ping-pong buffers and flag words are
+    all-gathered, and each rank maps its neighbours' (rank +- 1)."""
+    rank, world = dist.get_rank(), dist.get_world_size()
+    comm = Comm.peer(rank, world, buf0, buf1)
+    comm.attach(all_gather_bytes(comm.handles(), device))
+    return comm
 
 
 def slab(n0: int, rank: int, world: int):

@@ -116,3 +116,36 @@ def test_exchange_plan_and_slab():
     assert exchange_plan(16, 0, 4, 2) == [(1, (14, 16), (16, 18))]
     assert exchange_plan(16, 3, 4, 2) == [(2, (0, 2), (-2, 0))]
     assert exchange_plan(16, 1, 4, 2) == [(0, (0, 2), (-2, 0)), (2, (14, 16), (16, 18))]
+
+
+def _gather_worker(rank, world, port, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2103_09235_b200.api import Comm
+        from paper_2103_09235_b200.dist import all_gather_bytes
+        # a stand-in for this rank's 3 peer records (IPC handle + offset each)
+        rec = bytes((rank * 31 + i) % 256 for i in range(Comm.PEER_RECORD))
+        got = all_gather_bytes(rec)
+        ok = len(got) == world and all(
+            g == bytes((r * 31 + i) % 256 for i in range(Comm.PEER_RECORD)) for r, g in enumerate(got))
+        q.put((rank, ok))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_peer_records_all_gather(world):
+    """make_peer_comm's bootstrap: every rank gets every rank's peer records in
+    rank order (what stencil_comm_peer_attach expects)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_gather_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in ps:
+        p.start()
+    res = dict(q.get(timeout=120) for _ in ps)
+    for p in ps:
+        p.join(60)
+    assert all(res[r] for r in range(world)), res

@@ -70,8 +70,9 @@ def test_fullsize_sampled(key):
             assert err <= TOL[dtype], (key, m, lo, err)
 
 
-@pytest.mark.parametrize("key,G,m", [("c3", 4, 2), ("c4", 2, 2), ("c2", 8, 4)])
-def test_fullsize_dist_emulated_bitwise(key, G, m):
+@pytest.mark.parametrize("key,G,m,exchange", [("c3", 4, 2, "copies"), ("c4", 2, 2, "copies"), ("c2", 8, 4, "copies"),
+                                              ("c3", 4, 2, "peer"), ("c4", 4, 2, "peer"), ("c2", 8, 4, "peer")])
+def test_fullsize_dist_emulated_bitwise(key, G, m, exchange):
     from paper_2103_09235_b200 import Plan
     dims, shape, dtype, T, _ = CONFIGS[key]
     nd = len(dims)
@@ -91,7 +92,7 @@ def test_fullsize_dist_emulated_bitwise(key, G, m):
         ins.append(t)
         outs.append(plan.empty(layout=L))
         wss.append(plan.empty(layout=L))
-    plan.run_dist_emulated(ins, outs, T, m, halo, wss)
+    plan.run_dist_emulated(ins, outs, T, m, halo, wss, exchange=exchange)
     torch.cuda.synchronize()
     per = dims[0] // G
     for g in range(G):

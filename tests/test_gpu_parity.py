@@ -135,14 +135,17 @@ def test_dist_generator_and_layout():
             assert np.array_equal(plane.cpu().numpy(), full[zg + 1])
 
 
+@pytest.mark.parametrize("exchange", ["copies", "peer"])
 @pytest.mark.parametrize("dims,shape,dtype,m,stages,T,G", [
     ((64, 300), "box", "f32", 2, 1, 9, 2), ((64, 300), "box", "f32", 4, 2, 9, 4),
     ((48, 20, 70), "star", "f64", 2, 1, 7, 4), ((48, 20, 70), "box", "f64", 2, 2, 6, 2),
-    ((64, 300), "star", "f64", 1, 1, 5, 8)])
-def test_dist_emulated_bitwise_equals_single(dims, shape, dtype, m, stages, T, G):
-    """The slab-decomposed algorithm (all ranks on this GPU, exchange by D2D copies,
-    the same kernels and boxes as stencil_run_dist) is bitwise equal to 1 GPU
-    and within tolerance of the oracle."""
+    ((64, 300), "star", "f64", 1, 1, 5, 8), ((24, 20, 70), "star", "f64", 2, 1, 8, 4)])
+def test_dist_emulated_bitwise_equals_single(dims, shape, dtype, m, stages, T, G, exchange):
+    """The slab-decomposed algorithm (all ranks on this GPU, the same kernels and
+    boxes as stencil_run_dist) is bitwise equal to 1 GPU and within tolerance of
+    the oracle -- with the NCCL path's schedule (exchange by D2D copies) and with
+    the fused peer stores of NEXT-2 (the sweep kernel writes the neighbours'
+    ghost planes itself; band blocks included)."""
     nd = len(dims)
     k = len(oracle.taps(nd, 1, oracle.STAR if shape == "star" else oracle.BOX))
     w = synth.weights(k, 1)
@@ -161,7 +164,7 @@ def test_dist_emulated_bitwise_equals_single(dims, shape, dtype, m, stages, T, G
         ins.append(t)
         outs.append(plan.empty(layout=L))
         wss.append(plan.empty(layout=L))
-    plan.run_dist_emulated(ins, outs, T, m, halo, wss, stages=stages)
+    plan.run_dist_emulated(ins, outs, T, m, halo, wss, stages=stages, exchange=exchange)
     torch.cuda.synchronize()
     single = plan.interior_view(b).cpu().numpy()
     per = dims[0] // G
@@ -228,3 +231,35 @@ def test_parity_radius2(dims, shape, m, stages, dtype, boundary):
     got, ref, u0 = run_case_r(dims, 2, shape, dtype, 6, m, stages, boundary)
     err = np.max(np.abs(got - ref))
     assert err <= TOL[dtype] * np.max(np.abs(u0)), err
+
+
+def test_peer_comm_single_rank_api():
+    """The fused-exchange C-ABI on one GPU: create a peer comm over the two
+    ping-pong buffers, export its IPC records, attach (no neighbours with one
+    rank) and run through stencil_run_dist -- equal to stencil_run; a run with
+    other buffers than the registered pair is rejected."""
+    from paper_2103_09235_b200 import StencilError
+    from paper_2103_09235_b200.api import Comm
+    dims = (64, 300)
+    plan = _plan(dims, "box", "f64", synth.weights(9, 1))
+    L = plan.layout_dist(0, 1, 2)
+    a = plan.empty(layout=L)
+    plan.fill_random_dist(0, 1, 2, a, 2)
+    b, ws = plan.empty(layout=L), plan.empty(layout=L)
+    comm = Comm.peer(0, 1, b, ws)
+    rec = comm.handles()
+    assert len(rec) == Comm.PEER_RECORD
+    comm.attach([rec])
+    plan.run_dist(comm, a, b, 9, 2, 2, ws)
+    b2, ws2 = plan.empty(layout=L), plan.empty(layout=L)
+    plan.run_dist(comm, a, ws, 1, 1, 2, b)      # registered pair, swapped roles: allowed
+    with pytest.raises(StencilError):
+        plan.run_dist(comm, a, b2, 9, 2, 2, ws2)
+    torch.cuda.synchronize()
+    ref, refws = plan.empty(), plan.empty()
+    a1 = plan.empty()
+    plan.fill_random(a1, 2)
+    plan.run(a1, ref, 9, 2, workspace=refws)
+    torch.cuda.synchronize()
+    assert torch.equal(plan.interior_view(b, L), plan.interior_view(ref))
+    comm.close()
