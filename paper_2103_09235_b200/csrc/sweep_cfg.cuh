@@ -85,16 +85,33 @@ using Cfg2 = Cfg<T, 2, SHAPE, RR, Q, S, (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NTXH :
                  vxm2<SHAPE, Q, RR>(), (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_MINBH : SB_2D_MINB),
                  (vxm2<SHAPE, Q, RR>() > 1 && !plc2<Q, RR>() ? SB_ROT_2DH : SB_ROT_2D), SB_PINC_2D>;
 // The folded 3D star pass with Q = 2 (25 taps, C4 m=2) takes 4 output rows per
-// thread (more FMAs per shared-memory row), 2-plane slots and pinned
-// coefficients (measured 514 vs 458 GStencil/s); the rest use the defaults.
+// thread (more FMAs per shared-memory row) in a 64x32 tile (the y halo re-read
+// is 12.5% instead of 25%), 2-plane slots and pinned coefficients (measured
+// on one box: 520 vs 495 for the 64x16 tile, 458 for the default config).
 template <int SHAPE, int Q, int S>
 constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 // (radius-2 3D configs use the defaults: star2_3d is keyed on Q only for r = 1)
+#ifndef SB_S2_NTY
+#define SB_S2_NTY 8
+#endif
+#ifndef SB_S2_VY
+#define SB_S2_VY 4
+#endif
+#ifndef SB_S2_PB
+#define SB_S2_PB 2
+#endif
+#ifndef SB_S2_NSLOT
+#define SB_S2_NSLOT 3
+#endif
+#ifndef SB_S2_MINB
+#define SB_S2_MINB 1
+#endif
 template <typename T, int SHAPE, int Q, int S, int RR = 1>
-using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32, (star2_3d<SHAPE, Q, S>() ? 4 : SB_3D_NTY),
-                 (star2_3d<SHAPE, Q, S>() ? 4 : SB_3D_VY), (star2_3d<SHAPE, Q, S>() ? 2 : SB_3D_PB),
-                 (star2_3d<SHAPE, Q, S>() ? 3 : SB_3D_NSLOT), 1, (star2_3d<SHAPE, Q, S>() ? 3 : SB_3D_MINB),
-                 SB_ROT_3D, (star2_3d<SHAPE, Q, S>() ? 1 : SB_PINC_3D)>;
+using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32, (star2_3d<SHAPE, Q, S>() ? SB_S2_NTY : SB_3D_NTY),
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : SB_3D_VY), (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : SB_3D_PB),
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : SB_3D_NSLOT), 1,
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_MINB : SB_3D_MINB), SB_ROT_3D,
+                 (star2_3d<SHAPE, Q, S>() ? 1 : SB_PINC_3D)>;
 
 
 // 2D counterpart passes (NEXT-3): one pass of lambda^(Q) through CP
