@@ -106,11 +106,18 @@ constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 #ifndef SB_S2_MINB
 #define SB_S2_MINB 1
 #endif
+// The single 3D box step (27 taps, C5 m=1) takes 4 output rows per thread in a
+// 64x32 tile with 3 one-plane slots, 1 CTA/SM (measured 346 vs 318 GStencil/s
+// in one gpurun call; the same change costs 14% on the 7-tap star, which keeps
+// the defaults).
+template <int SHAPE, int Q, int S, int RR>
+constexpr bool box1_3d() { return SHAPE == STENCIL_BOX && Q == 1 && S == 1 && RR == 1; }
 template <typename T, int SHAPE, int Q, int S, int RR = 1>
 using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32, (star2_3d<SHAPE, Q, S>() ? SB_S2_NTY : SB_3D_NTY),
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : SB_3D_VY), (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : SB_3D_PB),
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : SB_3D_NSLOT), 1,
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_MINB : SB_3D_MINB), SB_ROT_3D,
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : box1_3d<SHAPE, Q, S, RR>() ? 4 : SB_3D_VY),
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : SB_3D_PB),
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : box1_3d<SHAPE, Q, S, RR>() ? 3 : SB_3D_NSLOT), 1,
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_MINB : box1_3d<SHAPE, Q, S, RR>() ? 1 : SB_3D_MINB), SB_ROT_3D,
                  (star2_3d<SHAPE, Q, S>() ? 1 : SB_PINC_3D)>;
 
 

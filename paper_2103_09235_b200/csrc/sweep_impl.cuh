@@ -1086,6 +1086,11 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
         double share = vol_total > 0 ? double(b.volume()) / double(vol_total) : 1.0;
         int64_t want = std::max<int64_t>(1, (int64_t)(target * share) / std::max<int64_t>(1, cols));
         if (C::ND == 3 && cols >= p->sm_count) want = 1;
+#ifdef SB_3D_ZSPLIT
+        // (tuning) z-chunks per column; segments are z-chunk-major, so CTAs sweep
+        // all columns of one z-range before the next and neighbours' halos meet in L2
+        if (C::ND == 3 && SB_3D_ZSPLIT > 0) want = SB_3D_ZSPLIT;
+#endif
         int64_t nch = std::min<int64_t>(want, std::max<int64_t>(1, zlen / 8));
         int64_t zc = (zlen + nch - 1) / nch;
         nch = (zlen + zc - 1) / zc;
