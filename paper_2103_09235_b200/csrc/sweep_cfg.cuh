@@ -55,7 +55,7 @@ namespace sb {
 // FMA-heavy passes (|supp lambda^(Q)| >= 25) give each thread more outputs so the
 // neighbourhood loads and per-row bookkeeping are amortised over more FMAs.
 #ifndef SB_STAR_HEAVY_Q
-#define SB_STAR_HEAVY_Q 4
+#define SB_STAR_HEAVY_Q 8
 #endif
 template <int SHAPE, int Q, int RR = 1>
 constexpr int vxm2() { return (SHAPE == STENCIL_BOX ? Q * RR >= 2 : Q * RR >= SB_STAR_HEAVY_Q) ? SB_2D_VXM_HEAVY : 1; }
