@@ -187,7 +187,9 @@ Variant choose_variant(Plan* p, int m) {
             red = (w + 2.0 * (s - 1) * q * p->r) / w;
             if (p->ndim == 3) red *= (64.0 + 2.0 * (s - 1) * q * p->r) / 64.0;
         }
-        double cost = s * support_size(p->ndim, p->shape, p->r, q) * red;
+        // + a fixed cost per on-chip hand-off, calibrated on B200 (C3 m=4: 2 passes of
+        // lambda^(2) 731 vs 4 single steps 623 GStencil/s although the latter has fewer FMAs)
+        double cost = s * support_size(p->ndim, p->shape, p->r, q) * red + 12.0 * (s - 1);
         if (cost < best_cost) { best_cost = cost; best = {q, s}; }
     }
     return best;

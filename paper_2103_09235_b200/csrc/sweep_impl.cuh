@@ -1134,7 +1134,10 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
     prm.sc.ctr = reinterpret_cast<unsigned int*>(static_cast<unsigned long long*>(p->sched) + p->sched_words - 2);
     prm.sc.epoch = p->epoch;
     prm.sc.nseg = (int)nseg;
-    prm.sc.chunk = std::max(2 * C::PB, 16);
+#ifndef SB_CHUNK
+#define SB_CHUNK 16
+#endif
+    prm.sc.chunk = std::max(2 * C::PB, SB_CHUNK);
     prm.sc.min_steal = std::max(2 * prm.sc.chunk, 4 * C::H + 8);
     int64_t tiles = std::min<int64_t>(nseg, target);   // persistent: one resident wave
     if (band_blocks > 0) tiles = std::max<int64_t>(tiles, std::min<int64_t>(band_blocks, target));
