@@ -112,13 +112,35 @@ constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 // the defaults).
 template <int SHAPE, int Q, int S, int RR>
 constexpr bool box1_3d() { return SHAPE == STENCIL_BOX && Q == 1 && S == 1 && RR == 1; }
+// two on-chip box steps (C5 m=2)
+#ifndef SB_B2_NTY
+#define SB_B2_NTY 8
+#endif
+#ifndef SB_B2_VY
+#define SB_B2_VY 2
+#endif
+#ifndef SB_B2_MINB
+#define SB_B2_MINB 2
+#endif
+#ifndef SB_B2_PINC
+#define SB_B2_PINC 0
+#endif
+#ifndef SB_B2_NSLOT
+#define SB_B2_NSLOT 4
+#endif
+template <int SHAPE, int Q, int S, int RR>
+constexpr bool box2s_3d() { return SHAPE == STENCIL_BOX && Q == 1 && S == 2 && RR == 1; }
 template <typename T, int SHAPE, int Q, int S, int RR = 1>
-using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32, (star2_3d<SHAPE, Q, S>() ? SB_S2_NTY : SB_3D_NTY),
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : box1_3d<SHAPE, Q, S, RR>() ? 4 : SB_3D_VY),
+using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32,
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NTY : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NTY : SB_3D_NTY),
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : box1_3d<SHAPE, Q, S, RR>() ? 4
+                                                    : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_VY : SB_3D_VY),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : SB_3D_PB),
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : box1_3d<SHAPE, Q, S, RR>() ? 3 : SB_3D_NSLOT), 1,
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_MINB : box1_3d<SHAPE, Q, S, RR>() ? 1 : SB_3D_MINB), SB_ROT_3D,
-                 (star2_3d<SHAPE, Q, S>() ? 1 : SB_PINC_3D)>;
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : box1_3d<SHAPE, Q, S, RR>() ? 3
+                                                       : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NSLOT : SB_3D_NSLOT), 1,
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_MINB : box1_3d<SHAPE, Q, S, RR>() ? 1
+                                                      : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_MINB : SB_3D_MINB),
+                 SB_ROT_3D, (star2_3d<SHAPE, Q, S>() ? 1 : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_PINC : SB_PINC_3D)>;
 
 
 // 2D counterpart passes (NEXT-3): one pass of lambda^(Q) through CP
