@@ -76,8 +76,11 @@ constexpr int vxm2() { return (SHAPE == STENCIL_BOX ? Q * RR >= 2 : Q * RR >= SB
 // branch-free phase loop; measured +7% on C3 m=2, +14% on C2 m=4 in 2 passes);
 // the 9-plane window of Q = 4 keeps 4-row slots (a 9-row slot would cost
 // occupancy and spill).
+#ifndef SB_PLC_MAXNW
+#define SB_PLC_MAXNW 5
+#endif
 template <int Q, int RR = 1>
-constexpr bool plc2() { return 2 * Q * RR + 1 <= 5; }
+constexpr bool plc2() { return 2 * Q * RR + 1 <= SB_PLC_MAXNW; }
 template <typename T, int SHAPE, int Q, int S, int RR = 1>
 using Cfg2 = Cfg<T, 2, SHAPE, RR, Q, S, (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NTXH : SB_2D_NTX), 1, 1,
                  (plc2<Q, RR>() ? 0 : SB_2D_PB),
