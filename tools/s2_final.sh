@@ -14,6 +14,9 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --c
 python tools/profile_sweep.py --config c2 --m 4 --sweeps 2 > gpurun_out/p_c2m4.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 1 -c 1 -o gpurun_out/prof_c2_m4 \
   python tools/profile_sweep.py --config c2 --m 4 --sweeps 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+python tools/profile_sweep.py --config c4 --m 2 --sweeps 2 > gpurun_out/p_c4m2.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 1 -c 1 -o gpurun_out/prof_c4_m2 \
+  python tools/profile_sweep.py --config c4 --m 2 --sweeps 2 > gpurun_out/ncu_full_c4.log 2>&1; echo "ncu full c4 rc=$?"
 python - <<'PY'
 import json
 for c in ['default','c1','c2','c3','c4','c5','c3u','reference']:
