@@ -154,6 +154,15 @@ int stencil_plan_fold_rank(stencil_plan plan, int m, int *rank, double *a, doubl
 int stencil_plan_set_counterparts(stencil_plan plan, int enable);
 
 /*
+ * Fault injection for tests (the mutation idea of S:464): add
+ * `delta` to entry `index` of the plan's cached lambda^(m) (dense layout of
+ * stencil_plan_fold_coeffs).  Every later run with fold_m = m uses the
+ * perturbed weights, so a parity check against the oracle must fail.
+ * Errors: EINVAL (NULL, m out of 1..STENCIL_MAX_FOLD, index out of range).
+ */
+int stencil_plan_perturb_fold(stencil_plan plan, int m, int64_t index, double delta);
+
+/*
  * The evaluation stencil_run(..., fold_m = m, stages = 0) chooses for the
  * main region (the GPU form of the profitability index Eq.3):
  * `stages` passes of lambda^(q) (m = q * stages); rank > 0 = one pass through

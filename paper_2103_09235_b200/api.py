@@ -136,6 +136,10 @@ class Plan:
                                                b.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), a.size))
         return rank.value, a[:rank.value].copy(), b[:rank.value].copy()
 
+    def perturb_fold(self, m: int, index: int, delta: float) -> None:
+        """Fault injection (tests): lambda^(m)[index] += delta for later runs."""
+        check(self._lib.stencil_plan_perturb_fold(self._h, int(m), int(index), float(delta)))
+
     def set_counterparts(self, enable: bool) -> None:
         check(self._lib.stencil_plan_set_counterparts(self._h, 1 if enable else 0))
 

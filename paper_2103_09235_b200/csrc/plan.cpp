@@ -387,6 +387,22 @@ int stencil_plan_fold_rank(stencil_plan plan, int m, int* rank, double* a, doubl
     return STENCIL_OK;
 }
 
+int stencil_plan_perturb_fold(stencil_plan plan, int m, int64_t index, double delta) {
+    if (!plan) return set_error(STENCIL_EINVAL, "NULL argument");
+    if (m < 1 || m > STENCIL_MAX_FOLD) return set_error(STENCIL_EINVAL, "bad fold_m");
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    std::vector<double>& lam = const_cast<std::vector<double>&>(folded(p, m));
+    if (index < 0 || index >= (int64_t)lam.size()) return set_error(STENCIL_EINVAL, "index out of range");
+    std::lock_guard<std::mutex> g(p->mu);
+    lam[(size_t)index] += delta;
+    auto it = p->lowrank.find(m);   // the counterparts derive from lambda: recompute on demand
+    if (it != p->lowrank.end()) {
+        delete it->second;
+        p->lowrank.erase(it);
+    }
+    return STENCIL_OK;
+}
+
 int stencil_plan_set_counterparts(stencil_plan plan, int enable) {
     if (!plan) return set_error(STENCIL_EINVAL, "NULL argument");
     reinterpret_cast<Plan*>(plan)->counterparts = enable != 0;

@@ -263,3 +263,25 @@ def test_peer_comm_single_rank_api():
     torch.cuda.synchronize()
     assert torch.equal(plan.interior_view(b, L), plan.interior_view(ref))
     comm.close()
+
+
+@pytest.mark.parametrize("dims,shape,dtype,m", [((70, 523), "star", "f64", 2), ((70, 523), "box", "f32", 2),
+                                                ((19, 37, 75), "star", "f64", 2), ((70, 523), "star", "f64", 4)])
+def test_fault_injection_is_caught(dims, shape, dtype, m):
+    """Perturbing one folded coefficient by 1e-6 (relative to the weights' scale)
+    must make the parity check fail: the tests see a wrong lambda^(m)."""
+    nd = len(dims)
+    offs = oracle.taps(nd, 1, oracle.STAR if shape == "star" else oracle.BOX)
+    w = synth.weights(len(offs), 1)
+    u0 = synth.u0_frame(dims, 1, 2)
+    ref = oracle.run(dims, 1, offs, w, u0, 8)
+    plan = _plan(dims, shape, dtype, w)
+    side = 2 * m + 1
+    center = (side ** nd) // 2
+    plan.perturb_fold(m, center, 1e-6 if dtype == "f64" else 1e-3)
+    a = plan.from_frame(u0)
+    b, ws = plan.empty(), plan.empty()
+    plan.run(a, b, 8, m, workspace=ws, stages=1)
+    torch.cuda.synchronize()
+    err = np.max(np.abs(plan.frame_view(b).cpu().double().numpy() - ref))
+    assert err > TOL[dtype] * np.max(np.abs(u0)), err
