@@ -9,6 +9,7 @@ static LaunchFn pick2(int q, int s) {
     if (q == 1 && s == 1) return launch_cfg<Cfg2<T, SHAPE, 1, 1>>;
     if (q == 2 && s == 1) return launch_cfg<Cfg2<T, SHAPE, 2, 1>>;
     if (q == 4 && s == 1) return launch_cfg<Cfg2<T, SHAPE, 4, 1>>;
+    if (q == 3 && s == 1) return launch_cfg<Cfg2<T, SHAPE, 3, 1>>;
     if (q == 1 && s == 2) return launch_cfg<Cfg2<T, SHAPE, 1, 2>>;
     if (q == 1 && s == 4) return launch_cfg<Cfg2<T, SHAPE, 1, 4>>;
     if (q == 2 && s == 2) return launch_cfg<Cfg2<T, SHAPE, 2, 2>>;

@@ -21,7 +21,7 @@ pytestmark = pytest.mark.gpu
 
 CONFIGS = {
     "c1": ((100000,), "star", "f64", 100, (1, 2)),
-    "c2": ((8192, 8192), "star", "f64", 200, (1, 2, 4)),
+    "c2": ((8192, 8192), "star", "f64", 200, (1, 2, 3, 4)),
     "c3": ((16384, 16384), "box", "f32", 200, (1, 2, 4)),
     "c4": ((512, 512, 512), "star", "f64", 100, (1, 2)),
     "c5": ((384, 768, 768), "box", "f64", 100, (1, 2)),

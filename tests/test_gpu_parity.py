@@ -41,7 +41,7 @@ def run_case(dims, shape, dtype, T, m, stages, seed_w=1, seed_u=2, u0=None, w=No
     return got, ref, u0, plan
 
 
-CASES_2D = [(m, s) for (m, s) in [(1, 1), (2, 1), (4, 1), (2, 2), (4, 2), (4, 4)]]
+CASES_2D = [(m, s) for (m, s) in [(1, 1), (2, 1), (3, 1), (4, 1), (2, 2), (4, 2), (4, 4)]]
 
 
 @pytest.mark.parametrize("shape", ["star", "box"])
