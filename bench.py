@@ -382,7 +382,7 @@ def run_ours(args):
     in_host = plan.empty("cpu", layout=L, pin_memory=True)
     out_host = plan.empty("cpu", layout=L, pin_memory=True)
     in_host.copy_(a.cpu())
-    ke = max(1, min(args.steps, 5))
+    ke = max(1, args.steps)          # as many steps as the timed region (same power-cap regime)
 
     def e2e_step():
         if world > 1:
@@ -394,14 +394,47 @@ def run_ours(args):
     e2e_step()
     torch.cuda.synchronize()
     barrier()
-    x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    x0.record(stream)
-    for _ in range(ke):
-        e2e_step()
-    x1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    e2e_ms = allmax(x0.elapsed_time(x1) / ke)
+    pipelined = world == 1
+    if pipelined:
+        # Steps overlap on the GPU's copy engines: the H2D of step k+1 and the D2H of
+        # step k-1 run while step k computes (two device buffer sets, one copy stream
+        # each way; the compute stays on one stream, every step still copies its whole
+        # input in and its whole result out).
+        sets = [(a, b, ws), (plan.empty(), plan.empty(), plan.empty())]
+        outs_h = [out_host, plan.empty("cpu", layout=L, pin_memory=True)]
+        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "comp", "out")}
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(s_in)
+        for k in range(ke):
+            j = k % 2
+            din, dout, dws = sets[j]
+            if k >= 2:
+                s_in.wait_event(ev["comp"][j])          # step k-2 finished reading din
+            with torch.cuda.stream(s_in):
+                din.copy_(in_host, non_blocking=True)
+            ev["in"][j].record(s_in)
+            stream.wait_event(ev["in"][j])
+            if k >= 2:
+                stream.wait_event(ev["out"][j])         # step k-2's result left dout
+            plan.run(din, dout, T, m, dws, args.stages)
+            ev["comp"][j].record(stream)
+            s_out.wait_event(ev["comp"][j])
+            with torch.cuda.stream(s_out):
+                outs_h[j].copy_(dout, non_blocking=True)
+            ev["out"][j].record(s_out)
+        x1.record(s_out)
+        torch.cuda.synchronize()
+        e2e_ms = x0.elapsed_time(x1) / ke
+    else:
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(ke):
+            e2e_step()
+        x1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = allmax(x0.elapsed_time(x1) / ke)
 
     if rank != 0:
         if world > 1:
@@ -453,7 +486,12 @@ def run_ours(args):
                        if args.stages == 0 and nd >= 2 else {"stages": args.stages or "auto"}},
             "gpu_launches": launches,
             "e2e": {"value": points * T / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
+                    "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": ke,
+                    "pipelined": pipelined,
+                    "how": ("pinned host -> device copy of the whole input frame, Plan.run, device -> pinned host "
+                            "copy of the whole result, every step; copies of neighbouring steps overlap the "
+                            "compute on the copy engines" if pipelined else
+                            "stencil_run_host / run_dist with H2D and D2H copies, every step, one stream")},
             "roofline": roof,
             "clocks": cl,
             "variants": variants, "variants_note": variants_note}
