@@ -184,6 +184,10 @@ __device__ __forceinline__ uint32_t pin(uint32_t v) {
 }
 __device__ __forceinline__ float fmaT(float a, float b, float c) { return __fmaf_rn(a, b, c); }
 
+#ifndef SB_FOLD_OXMAJOR
+#define SB_FOLD_OXMAJOR 0
+#endif
+
 template <class C>
 struct Consumer {
     using T = typename C::T;
@@ -229,6 +233,29 @@ struct Consumer {
         for (int rr = 0; rr < C::NR; ++rr) {
             T row[C::NV * C::VEC];
             ld(rr, row);
+#if SB_FOLD_OXMAJOR
+            // x offset outermost: consecutive FMAs update different accumulators
+            // (the per-accumulator order of contributions is unchanged: bitwise equal)
+#pragma unroll
+            for (int ox = -RQ; ox <= RQ; ++ox)
+#pragma unroll
+                for (int k = 0; k < NW; ++k) {
+                    const int oz = RQ - k;
+                    const int idx = pmod(PH - J * RQ - RQ + k, NW);
+#pragma unroll
+                    for (int oy = -RQY; oy <= RQY; ++oy) {
+                        const int vy = rr - oy - RQY;
+                        if (vy < 0 || vy >= C::VY) continue;
+                        if (!in_support<C::SHAPE, C::RR, C::Q>(oz, oy, ox)) continue;
+                        const int ci = C::ND == 3 ? ((oz + RQ) * (2 * RQY + 1) + (oy + RQY)) * (2 * RQ + 1) + (ox + RQ)
+                                                  : (oz + RQ) * (2 * RQ + 1) + (ox + RQ);
+                        const T c = coef[ci];
+#pragma unroll
+                        for (int vx = 0; vx < C::VX; ++vx)
+                            acc[J][idx][vy][vx] = fmaT(c, row[vx + ox + C::PX], acc[J][idx][vy][vx]);
+                    }
+                }
+#else
 #pragma unroll
             for (int k = 0; k < NW; ++k) {
                 const int oz = RQ - k;
@@ -249,6 +276,7 @@ struct Consumer {
                     }
                 }
             }
+#endif
         }
     }
 };
