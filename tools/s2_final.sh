@@ -11,9 +11,9 @@ done
 timeout 300 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.json 2> gpurun_out/bench_reference.err; echo "ref rc=$?"
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/launches_c2.csv \
   python bench.py --steps 2 --warmup 1 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
-python tools/profile_sweep.py --config c2 --m 4 --sweeps 2 > gpurun_out/p_c2m4.log 2>&1 && \
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 1 -c 1 -o gpurun_out/prof_c2_m4 \
-  python tools/profile_sweep.py --config c2 --m 4 --sweeps 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+python tools/profile_sweep.py --config c2 --m 3 --sweeps 2 > gpurun_out/p_c2m3.log 2>&1 && \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 1 -c 1 -o gpurun_out/prof_c2_m3 \
+  python tools/profile_sweep.py --config c2 --m 3 --sweeps 2 > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
 python tools/profile_sweep.py --config c4 --m 2 --sweeps 2 > gpurun_out/p_c4m2.log 2>&1 && \
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:sweep_kernel -s 1 -c 1 -o gpurun_out/prof_c4_m2 \
   python tools/profile_sweep.py --config c4 --m 2 --sweeps 2 > gpurun_out/ncu_full_c4.log 2>&1; echo "ncu full c4 rc=$?"
