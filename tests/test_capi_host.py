@@ -180,3 +180,29 @@ def test_counterparts_can_be_disabled():
     assert p.variant(2)[2] == 1
     p.set_counterparts(False)
     assert p.variant(2)[2] == 0
+
+
+def test_new_entry_points_validate_arguments():
+    """Argument checks of the NEXT-2/3 entry points that need no GPU."""
+    import ctypes
+    lib = _lib.load()
+    p3 = Plan((8, 8, 8), 1, "star", synth.weights(7, 1))
+    with pytest.raises(StencilError):
+        p3.fold_rank(2)                                  # counterparts are 2D
+    p2 = Plan((16, 16), 1, "box", synth.weights(9, 1))
+    with pytest.raises(StencilError):
+        p2.fold_rank(0)
+    with pytest.raises(StencilError):
+        p2.variant(0)
+    with pytest.raises(StencilError):
+        p2.perturb_fold(2, 25, 1.0)                      # 5x5 = 25 entries: index 25 is out of range
+    p2.perturb_fold(2, 12, 0.0)                          # in range, no-op
+    r = ctypes.c_int()
+    assert lib.stencil_plan_variant(p2._h, 2, None, None, None) == -1
+    assert lib.stencil_plan_fold_rank(p2._h, 2, None, None, None, 0) == -1
+    h = ctypes.c_void_p()
+    assert lib.stencil_comm_create_peer(ctypes.byref(h), 0, 2, None, None) == -1
+    assert lib.stencil_comm_create_peer(ctypes.byref(h), 2, 2, ctypes.c_void_p(256), ctypes.c_void_p(512)) == -1
+    assert lib.stencil_comm_peer_handles(None, ctypes.create_string_buffer(216)) == -1
+    assert lib.stencil_comm_peer_attach(None, ctypes.create_string_buffer(216)) == -1
+    del r
