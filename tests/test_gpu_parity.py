@@ -285,3 +285,11 @@ def test_fault_injection_is_caught(dims, shape, dtype, m):
     torch.cuda.synchronize()
     err = np.max(np.abs(plan.frame_view(b).cpu().double().numpy() - ref))
     assert err > TOL[dtype] * np.max(np.abs(u0)), err
+
+
+@pytest.mark.parametrize("r,m,T,boundary", [(4, 8, 17, "fixed"), (3, 6, 13, "fixed"), (3, 6, 13, "periodic"),
+                                            (4, 4, 9, "periodic"), (2, 8, 21, "fixed")])
+def test_parity_1d_wide_folds(r, m, T, boundary):
+    """1D folds of radius m*r > 16 (32 cells per lane) and up to STENCIL_MAX_FOLD."""
+    got, ref, u0 = run_case_r((4000,), r, "star", "f64", T, m, 0, boundary)
+    assert np.max(np.abs(got - ref)) <= 1e-11 * np.max(np.abs(u0))
