@@ -13,10 +13,20 @@
 #include <cstring>
 #include <mutex>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.hpp"
 #include "sweep_params.cuh"
 
 namespace sb {
+
+// ------------------------------------------------------------------ tracing
+// NVTX ranges (header-only NVTX 3: free unless a profiler is attached) around
+// every run and every sweep, so nsys/ncu timelines show the library's phases.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+};
 
 // ------------------------------------------------------------------ timing
 static void* take_event(Plan* p) {
@@ -99,6 +109,8 @@ struct SweepSpec {
 static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, const SweepSpec& s,
                          int64_t z0, int64_t z1, void* stream, void* peer_lo = nullptr, void* peer_hi = nullptr,
                          int peer_h = 0) {
+    NvtxRange nv(s.v.rank > 0 ? "stencil sweep (counterparts)" : s.v.stages > 1 ? "stencil sweep (on-chip stages)"
+                                                                               : "stencil sweep (folded)");
     Box mainb;
     std::vector<Box> band;
     split_band(L, s.m, &mainb, &band);
@@ -237,6 +249,7 @@ static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t 
 }
 
 int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages, void* ws, void* stream) {
+    NvtxRange nv("stencil_run");
     int rc = check_run_args(p, in, out, T, m, ws);
     if (rc) return rc;
     rc = ensure_device(p);
@@ -776,6 +789,7 @@ int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void* buf, int h
 
 int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local, void* out_local, int64_t T,
                      int fold_m, int stages, int halo, void* workspace, void* stream) {
+    NvtxRange nv("stencil_run_dist");
     Plan* p = reinterpret_cast<Plan*>(plan);
     if (!comm) return set_error(STENCIL_EINVAL, "comm is NULL");
     int rc = check_run_args(p, in_local, out_local, T, fold_m, workspace);
