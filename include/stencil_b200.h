@@ -154,6 +154,15 @@ int stencil_plan_fold_rank(stencil_plan plan, int m, int *rank, double *a, doubl
 int stencil_plan_set_counterparts(stencil_plan plan, int enable);
 
 /*
+ * fold_m = 0 in stencil_run / stencil_run_ex / stencil_run_host /
+ * stencil_run_dist means "auto": this fold, chosen per family from the B200
+ * measurements: 1D 2; 2D star 3;
+ * 2D box 2, or 4 when lambda^(4) has a counterpart decomposition of rank <= 2;
+ * 3D star 2; 3D box 1; radius > 1: 1.  Errors: EINVAL (NULL).
+ */
+int stencil_plan_auto_fold(stencil_plan plan, int *fold_m);
+
+/*
  * Fault injection for tests (the mutation idea of S:464): add
  * `delta` to entry `index` of the plan's cached lambda^(m) (dense layout of
  * stencil_plan_fold_coeffs).  Every later run with fold_m = m uses the
@@ -182,7 +191,8 @@ int stencil_workspace_size(stencil_plan plan, int64_t *bytes);
 int stencil_fill_random(stencil_plan plan, void *buf, uint64_t seed, void *stream);
 
 /*
- * Run T time steps: out = S^T(in), with fold_m steps per sweep (Eq.2):
+ * Run T time steps: out = S^T(in), with fold_m steps per sweep (Eq.2; 0 = auto,
+ * stencil_plan_auto_fold):
  *   floor(T / fold_m) folded sweeps, then T mod fold_m single steps
  *   (R10).  Jacobi ping-pong between `out` and `workspace`
  *    arranged so the last sweep writes `out`; `in` is never written.

@@ -35,6 +35,7 @@ SIGNATURES = {
     "stencil_plan_fold_rank": (c_int, [c_vp, c_int, ctypes.POINTER(c_int), c_dp, c_dp, c_i64]),
     "stencil_plan_set_counterparts": (c_int, [c_vp, c_int]),
     "stencil_plan_perturb_fold": (c_int, [c_vp, c_int, c_i64, ctypes.c_double]),
+    "stencil_plan_auto_fold": (c_int, [c_vp, ctypes.POINTER(c_int)]),
     "stencil_plan_variant": (c_int, [c_vp, c_int, ctypes.POINTER(c_int), ctypes.POINTER(c_int),
                                      ctypes.POINTER(c_int)]),
     "stencil_workspace_size": (c_int, [c_vp, ctypes.POINTER(c_i64)]),

@@ -140,6 +140,12 @@ class Plan:
         """Fault injection (tests): lambda^(m)[index] += delta for later runs."""
         check(self._lib.stencil_plan_perturb_fold(self._h, int(m), int(index), float(delta)))
 
+    def auto_fold(self) -> int:
+        """The fold_m a run with fold_m = 0 uses (stencil_plan_auto_fold)."""
+        m = ctypes.c_int()
+        check(self._lib.stencil_plan_auto_fold(self._h, ctypes.byref(m)))
+        return m.value
+
     def set_counterparts(self, enable: bool) -> None:
         check(self._lib.stencil_plan_set_counterparts(self._h, 1 if enable else 0))
 

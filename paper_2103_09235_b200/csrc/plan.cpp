@@ -278,6 +278,22 @@ void to_public(const Layout3& L, stencil_layout* out) {
     out->global_offset0 = L.gofs0;
 }
 
+// fold_m = 0 ("auto"): per family, the fold that keeps the folded pass near the
+// HBM roofline without making it FMA-bound (measured for the
+// five BASELINE configs and the uniform 2D9P).
+int auto_fold(Plan* p) {
+    if (p->ndim == 1) return 2;
+    if (p->ndim == 2 && p->r == 1) {
+        if (p->counterparts && lowrank(p, 4).rank >= 1 && lowrank(p, 4).rank <= STENCIL_MAX_COUNTERPARTS &&
+            2 * 9 * lowrank(p, 4).rank < support_size(2, p->shape, 1, 4))
+            return 4;                                    // counterparts: 18 FMAs per point for 4 steps
+        if (p->shape == STENCIL_STAR) return 3;
+        return 2;
+    }
+    if (p->ndim == 3 && p->r == 1) return p->shape == STENCIL_STAR ? 2 : 1;
+    return 1;
+}
+
 }  // namespace sb
 
 using namespace sb;
@@ -400,6 +416,12 @@ int stencil_plan_perturb_fold(stencil_plan plan, int m, int64_t index, double de
         delete it->second;
         p->lowrank.erase(it);
     }
+    return STENCIL_OK;
+}
+
+int stencil_plan_auto_fold(stencil_plan plan, int* fold_m) {
+    if (!plan || !fold_m) return set_error(STENCIL_EINVAL, "NULL argument");
+    *fold_m = sb::auto_fold(reinterpret_cast<Plan*>(plan));
     return STENCIL_OK;
 }
 

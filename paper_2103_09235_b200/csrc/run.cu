@@ -250,6 +250,7 @@ static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t 
 
 int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages, void* ws, void* stream) {
     NvtxRange nv("stencil_run");
+    if (p && m == 0) m = auto_fold(p);
     int rc = check_run_args(p, in, out, T, m, ws);
     if (rc) return rc;
     rc = ensure_device(p);
@@ -790,6 +791,7 @@ int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void* buf, int h
 int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local, void* out_local, int64_t T,
                      int fold_m, int stages, int halo, void* workspace, void* stream) {
     NvtxRange nv("stencil_run_dist");
+    if (plan && fold_m == 0) fold_m = auto_fold(reinterpret_cast<Plan*>(plan));
     Plan* p = reinterpret_cast<Plan*>(plan);
     if (!comm) return set_error(STENCIL_EINVAL, "comm is NULL");
     int rc = check_run_args(p, in_local, out_local, T, fold_m, workspace);

@@ -206,3 +206,14 @@ def test_new_entry_points_validate_arguments():
     assert lib.stencil_comm_peer_handles(None, ctypes.create_string_buffer(216)) == -1
     assert lib.stencil_comm_peer_attach(None, ctypes.create_string_buffer(216)) == -1
     del r
+
+
+def test_auto_fold_table():
+    """fold_m = 0 (auto): the measured-best fold per family."""
+    assert Plan((100,), 1, "star", synth.weights(3, 1)).auto_fold() == 2
+    assert Plan((64, 64), 1, "star", synth.weights(5, 1)).auto_fold() == 3
+    assert Plan((64, 64), 1, "star", synth.weights(5, 1), dtype="f32").auto_fold() == 3
+    assert Plan((64, 64), 1, "box", synth.weights(9, 1), dtype="f32").auto_fold() == 2
+    assert Plan((64, 64), 1, "box", [1.0 / 9] * 9, dtype="f32").auto_fold() == 4      # counterparts
+    assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1)).auto_fold() == 2
+    assert Plan((16, 16, 16), 1, "box", synth.weights(27, 1)).auto_fold() == 1

@@ -321,3 +321,20 @@ def test_resume_is_the_semigroup(dims, shape, dtype, m):
     torch.cuda.synchronize()
     err = (plan.frame_view(full).double() - plan.frame_view(res).double()).abs().max().item()
     assert err <= TOL[dtype]
+
+
+@pytest.mark.parametrize("dims,shape,dtype", [((70, 523), "star", "f64"), ((19, 37, 75), "box", "f64"),
+                                              ((1000,), "star", "f64")])
+def test_auto_fold_run(dims, shape, dtype):
+    """fold_m = 0 runs the plan's auto fold and matches the oracle."""
+    nd = len(dims)
+    offs = oracle.taps(nd, 1, oracle.STAR if shape == "star" else oracle.BOX)
+    w = synth.weights(len(offs), 1)
+    u0 = synth.u0_frame(dims, 1, 2)
+    ref = oracle.run(dims, 1, offs, w, u0, 9)
+    plan = _plan(dims, shape, dtype, w)
+    a = plan.from_frame(u0)
+    b, ws = plan.empty(), plan.empty()
+    plan.run(a, b, 9, 0, workspace=ws)
+    torch.cuda.synchronize()
+    assert np.max(np.abs(plan.frame_view(b).cpu().double().numpy() - ref)) <= TOL[dtype] * np.max(np.abs(u0))
