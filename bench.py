@@ -42,7 +42,7 @@ CONFIGS = {
     "c1": dict(name="1D3P heat fp64 N=100000 T=100", dims=(100000,), shape="star", dtype="f64", T=100, ms=(1, 2),
                best_m=2),
     # fold_m = 3 is not in BASELINE's list {1, 2, 4} for this config; the folding works for
-    # any m (T = 200 = 66 folded sweeps + 2 single steps, R10) and m = 3 balances the
+    # any m (T = 200 = 66 sweeps of lambda^(3) + one of lambda^(2), R10) and m = 3 balances the
     # 25-tap fold against HBM: 0.77-0.83 of the HBM roofline (m = 4: 0.58) at the same
     # throughput within 2% (983 vs 953 in short runs; 918 vs 938 in 20-step runs, where
     # m = 3's higher HBM power pulls the SM clock to ~1.7 GHz under sw_power_cap)

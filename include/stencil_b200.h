@@ -193,7 +193,7 @@ int stencil_fill_random(stencil_plan plan, void *buf, uint64_t seed, void *strea
 /*
  * Run T time steps: out = S^T(in), with fold_m steps per sweep (Eq.2; 0 = auto,
  * stencil_plan_auto_fold):
- *   floor(T / fold_m) folded sweeps, then T mod fold_m single steps
+ *   floor(T / fold_m) folded sweeps, then one sweep of fold T mod fold_m
  *   (R10).  Jacobi ping-pong between `out` and `workspace`
  *    arranged so the last sweep writes `out`; `in` is never written.
  *   T = 0 copies in -> out.  Every sweep = the folded interior sweep plus the

@@ -186,6 +186,27 @@ static int resolve_variant(Plan* p, int m, int stages, Variant* v) {
     return STENCIL_OK;
 }
 
+// R10 refined: T = nf * m + nr steps run as nf sweeps of lambda^(m) and, when
+// nr > 1, ONE sweep of lambda^(nr) (one HBM pass instead of nr); nr single
+// steps only when no evaluation of fold nr is compiled.
+static void remainder_plan(Plan* p, int64_t T, int m, int64_t* n, int* mr, Variant* vr) {
+    const int64_t nf = T / m, nr = T % m;
+    *mr = 1;
+    *vr = Variant{1, 1};
+    if (nr > 1) {
+        Variant v;
+        const std::string keep = stencil_last_error();
+        if (resolve_variant(p, (int)nr, 0, &v) == STENCIL_OK) {
+            *mr = (int)nr;
+            *vr = v;
+            *n = nf + 1;
+            return;
+        }
+        set_error(STENCIL_OK, keep);   // the fallback is not an error
+    }
+    *n = nf + nr;
+}
+
 static bool misaligned(const void* ptr) { return (reinterpret_cast<uintptr_t>(ptr) & 127) != 0; }
 
 static int check_run_args(Plan* p, const void* in, void* out, int64_t T, int m, void* ws) {
@@ -266,7 +287,11 @@ int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages,
     Variant v;
     rc = resolve_variant(p, m, stages, &v);
     if (rc) return rc;
-    const int64_t nf = T / m, nr = T % m, n = nf + nr;
+    const int64_t nf = T / m;
+    int64_t n;
+    int mr;
+    Variant vr;
+    remainder_plan(p, T, m, &n, &mr, &vr);
     if (L.wrap) {
         // PERIODIC (NEXT-4): copy `in` (never written) into the buffer the
         // ping-pong starts from, fill its ghosts from the wrapped interior, then
@@ -283,8 +308,8 @@ int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages,
         launches += rc;
         for (int64_t j = 1; j <= n; ++j) {
             SweepSpec s;
-            s.m = j <= nf ? m : 1;
-            s.v = j <= nf ? v : Variant{1, 1};
+            s.m = j <= nf ? m : mr;
+            s.v = j <= nf ? v : vr;
             const void* src = bufs[(n - j + 1) % 2];
             void* dst = bufs[(n - j) % 2];
             rc = enqueue_sweep(p, L, src, dst, s, 0, L.n[0], stream);
@@ -310,8 +335,8 @@ int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages,
     void* bufs[2] = {out, ws};
     for (int64_t j = 1; j <= n; ++j) {
         SweepSpec s;
-        s.m = j <= nf ? m : 1;
-        s.v = j <= nf ? v : Variant{1, 1};
+        s.m = j <= nf ? m : mr;
+        s.v = j <= nf ? v : vr;
         const void* src = j == 1 ? in : bufs[(n - j + 1) % 2];
         void* dst = bufs[(n - j) % 2];
         rc = enqueue_sweep(p, L, src, dst, s, 0, L.n[0], stream);
@@ -475,7 +500,8 @@ static size_t plane_bytes(const Layout3& L) { return (size_t)L.stride[0] * L.esi
 // were written by the neighbours' sweep j, and a neighbour's sweep j+1 writes
 // into the buffer this rank read during sweep j.
 static int run_dist_peer(sb::Plan* p, stencil_comm_s* c, const sb::Layout3& L, const void* in_local, void* out_local,
-                         void* ws, int64_t n, int64_t nf, int fold_m, sb::Variant v, int64_t hx, void* stream) {
+                         void* ws, int64_t n, int64_t nf, int fold_m, sb::Variant v, int mr, sb::Variant vr, int64_t hx,
+                         void* stream) {
     using namespace sb;
     if (!((out_local == c->buf[0] && (n < 2 || ws == c->buf[1])) ||
           (out_local == c->buf[1] && (n < 2 || ws == c->buf[0]))))
@@ -499,8 +525,8 @@ static int run_dist_peer(sb::Plan* p, stencil_comm_s* c, const sb::Layout3& L, c
     void* bufs[2] = {out_local, ws};
     for (int64_t j = 1; j <= n; ++j) {
         SweepSpec s;
-        s.m = j <= nf ? fold_m : 1;
-        s.v = j <= nf ? v : Variant{1, 1};
+        s.m = j <= nf ? fold_m : mr;
+        s.v = j <= nf ? v : vr;
         const void* src = j == 1 ? in_local : bufs[(n - j + 1) % 2];
         const int di = (int)((n - j) % 2);           // 0 = out, 1 = ws
         const int reg = di == 0 ? bo : 1 - bo;       // registered index of dst
@@ -809,10 +835,15 @@ int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local,
     Variant v;
     rc = resolve_variant(p, fold_m, stages, &v);
     if (rc) return rc;
-    const int64_t nf = T / fold_m, nr = T % fold_m, n = nf + nr;
+    const int64_t nf = T / fold_m;
+    int64_t n;
+    int mr;
+    Variant vr;
+    remainder_plan(p, T, fold_m, &n, &mr, &vr);
     if (n >= 2 && !workspace) return set_error(STENCIL_EINVAL, "workspace required");
     const int64_t hx = (int64_t)fold_m * p->r;
-    if (comm->peer) return run_dist_peer(p, comm, L, in_local, out_local, workspace, n, nf, fold_m, v, hx, stream);
+    if (comm->peer)
+        return run_dist_peer(p, comm, L, in_local, out_local, workspace, n, nf, fold_m, v, mr, vr, hx, stream);
     int launches = 0;
     rc = launch_ring_copy(p, in_local, out_local, &L, stream);
     if (rc < 0) return rc;
@@ -825,8 +856,8 @@ int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local,
     void* bufs[2] = {out_local, workspace};
     for (int64_t j = 1; j <= n; ++j) {
         SweepSpec s;
-        s.m = j <= nf ? fold_m : 1;
-        s.v = j <= nf ? v : Variant{1, 1};
+        s.m = j <= nf ? fold_m : mr;
+        s.v = j <= nf ? v : vr;
         const void* src = j == 1 ? in_local : bufs[(n - j + 1) % 2];
         void* dst = bufs[(n - j) % 2];
         rc = sweep_phase(p, L, src, dst, s, comm->rank, comm->nranks, hx, 0, stream);
@@ -876,7 +907,11 @@ int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void* const* 
     Variant v;
     rc = resolve_variant(p, fold_m, stages, &v);
     if (rc) return rc;
-    const int64_t nf = T / fold_m, nr = T % fold_m, n = nf + nr;
+    const int64_t nf = T / fold_m;
+    int64_t n;
+    int mr;
+    Variant vr;
+    remainder_plan(p, T, fold_m, &n, &mr, &vr);
     if (n >= 2 && !workspaces) return set_error(STENCIL_EINVAL, "workspaces required");
     const int64_t hx = (int64_t)fold_m * p->r;
     int launches = 0;
@@ -896,8 +931,8 @@ int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void* const* 
         // ranks run one after another on one stream, so no flags are needed)
         for (int64_t j = 1; j <= n; ++j) {
             SweepSpec s;
-            s.m = j <= nf ? fold_m : 1;
-            s.v = j <= nf ? v : Variant{1, 1};
+            s.m = j <= nf ? fold_m : mr;
+            s.v = j <= nf ? v : vr;
             std::vector<void*> dsts(nranks);
             for (int g = 0; g < nranks; ++g) {
                 void* bufs[2] = {out_locals[g], workspaces ? workspaces[g] : nullptr};
@@ -921,8 +956,8 @@ int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void* const* 
     }
     for (int64_t j = 1; j <= n; ++j) {
         SweepSpec s;
-        s.m = j <= nf ? fold_m : 1;
-        s.v = j <= nf ? v : Variant{1, 1};
+        s.m = j <= nf ? fold_m : mr;
+        s.v = j <= nf ? v : vr;
         std::vector<const void*> srcs(nranks);
         std::vector<void*> dsts(nranks);
         for (int g = 0; g < nranks; ++g) {
