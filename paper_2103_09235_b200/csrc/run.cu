@@ -284,9 +284,11 @@ int run_single(Plan* p, const void* in, void* out, int64_t T, int m, int stages,
         return e == cudaSuccess ? STENCIL_OK : cuda_error(e, "cudaMemcpyAsync");
     }
     if (p->ndim == 1) return run_1d(p, L, in, out, T, m, stages, ws, stream);
-    Variant v;
-    rc = resolve_variant(p, m, stages, &v);
-    if (rc) return rc;
+    Variant v{1, 1};
+    if (T >= m) {   // (T < m: only the remainder sweep runs)
+        rc = resolve_variant(p, m, stages, &v);
+        if (rc) return rc;
+    }
     const int64_t nf = T / m;
     int64_t n;
     int mr;
@@ -832,9 +834,11 @@ int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local,
         cudaError_t e = cudaMemcpyAsync(out_local, in_local, L.bytes, cudaMemcpyDeviceToDevice, st);
         return e == cudaSuccess ? STENCIL_OK : cuda_error(e, "cudaMemcpyAsync");
     }
-    Variant v;
-    rc = resolve_variant(p, fold_m, stages, &v);
-    if (rc) return rc;
+    Variant v{1, 1};
+    if (T >= fold_m) {   // (T < fold_m: only the remainder sweep runs)
+        rc = resolve_variant(p, fold_m, stages, &v);
+        if (rc) return rc;
+    }
     const int64_t nf = T / fold_m;
     int64_t n;
     int mr;
@@ -904,9 +908,11 @@ int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void* const* 
         }
         return STENCIL_OK;
     }
-    Variant v;
-    rc = resolve_variant(p, fold_m, stages, &v);
-    if (rc) return rc;
+    Variant v{1, 1};
+    if (T >= fold_m) {   // (T < fold_m: only the remainder sweep runs)
+        rc = resolve_variant(p, fold_m, stages, &v);
+        if (rc) return rc;
+    }
     const int64_t nf = T / fold_m;
     int64_t n;
     int mr;

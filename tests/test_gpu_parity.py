@@ -338,3 +338,21 @@ def test_auto_fold_run(dims, shape, dtype):
     plan.run(a, b, 9, 0, workspace=ws)
     torch.cuda.synchronize()
     assert np.max(np.abs(plan.frame_view(b).cpu().double().numpy() - ref)) <= TOL[dtype] * np.max(np.abs(u0))
+
+
+@pytest.mark.parametrize("dims,shape,dtype,T,m", [
+    ((70, 523), "star", "f64", 3, 4), ((70, 523), "box", "f32", 7, 4), ((70, 523), "star", "f64", 11, 4),
+    ((19, 37, 75), "star", "f64", 3, 4), ((19, 37, 75), "box", "f64", 5, 2), ((19, 37, 75), "star", "f64", 1, 2)])
+def test_remainder_sweeps(dims, shape, dtype, T, m):
+    """T mod m != 0 (R10): the remainder runs as one sweep of lambda^(T mod m) where
+    that fold is compiled (2D: 3 -> lambda^(3)), else as single steps (3D: 3);
+    T < m has no full sweep at all (so 3D T=3, m=4 runs although no 3D
+    evaluation of fold 4 is compiled)."""
+    got, ref, u0, _ = run_case(dims, shape, dtype, T, m, 0)
+    assert np.max(np.abs(got - ref)) <= TOL[dtype] * np.max(np.abs(u0))
+
+
+def test_uncompiled_fold_is_unsupported():
+    from paper_2103_09235_b200 import StencilError
+    with pytest.raises(StencilError):
+        run_case((19, 37, 75), "box", "f64", 7, 4, 0)      # 3D fold 4: not compiled
