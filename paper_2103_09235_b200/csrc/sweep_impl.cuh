@@ -127,6 +127,9 @@ __host__ __device__ constexpr bool in_support(int oz, int oy, int ox) {
 
 __host__ __device__ constexpr int pmod(int a, int n) { return ((a % n) + n) % n; }
 
+#ifndef SB_STORE_CS
+#define SB_STORE_CS 0
+#endif
 template <typename T>
 struct VecT;
 template <>
@@ -143,6 +146,15 @@ struct VecT<double> {
     }
     static __device__ __forceinline__ void st(double* p, const double* in) {
         *reinterpret_cast<double2*>(p) = make_double2(in[0], in[1]);
+    }
+    // global output store; SB_STORE_CS: streaming (evict-first) so the written
+    // planes do not displace the input planes neighbouring tiles still need in L2
+    static __device__ __forceinline__ void stg(double* p, const double* in) {
+#if SB_STORE_CS
+        __stcs(reinterpret_cast<double2*>(p), make_double2(in[0], in[1]));
+#else
+        *reinterpret_cast<double2*>(p) = make_double2(in[0], in[1]);
+#endif
     }
 };
 template <>
@@ -161,6 +173,13 @@ struct VecT<float> {
     }
     static __device__ __forceinline__ void st(float* p, const float* in) {
         *reinterpret_cast<float4*>(p) = make_float4(in[0], in[1], in[2], in[3]);
+    }
+    static __device__ __forceinline__ void stg(float* p, const float* in) {
+#if SB_STORE_CS
+        __stcs(reinterpret_cast<float4*>(p), make_float4(in[0], in[1], in[2], in[3]));
+#else
+        *reinterpret_cast<float4*>(p) = make_float4(in[0], in[1], in[2], in[3]);
+#endif
     }
 };
 
@@ -846,7 +865,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
 #pragma unroll
                             for (int mm = 0; mm < C::VX / C::VEC; ++mm) {
                                 if (vmask & (1u << mm)) {
-                                    VecT<T>::st(op + mm * C::VEC, &cs.acc[C::S - 1][dn][vy][mm * C::VEC]);
+                                    VecT<T>::stg(op + mm * C::VEC, &cs.acc[C::S - 1][dn][vy][mm * C::VEC]);
                                 } else {
 #pragma unroll
                                     for (int e = 0; e < C::VEC; ++e) {
