@@ -32,7 +32,10 @@
  *    plain host memory, owned by the caller.
  *  - `stream` is a cudaStream_t (NULL = legacy default stream).  Runs are
  *    asynchronous on it; kernel faults surface at the caller's next
- *    synchronisation, as with any CUDA library.
+ *    synchronisation, as with any CUDA library.  A plan owns device scratch
+ *    for its sweep schedule, so the runs of ONE plan must be ordered (one
+ *    stream, or streams synchronised by the caller); different plans run
+ *    concurrently.  A plan is not thread-safe for concurrent calls.
  *  - Axes are listed slowest first (z, y, x); x has unit stride.
  */
 #ifndef STENCIL_B200_H
