@@ -113,7 +113,11 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
                                                                                : "stencil sweep (folded)");
     Box mainb;
     std::vector<Box> band;
-    split_band(L, s.m, &mainb, &band);
+    // The on-chip stepwise block (Q = 1, S = m stages) is exact up to the FIXED
+    // faces by itself: intermediate ring cells are reloaded from u0 (R1), so it
+    // takes the whole interior and no band is needed.
+    const bool stepwise_exact = s.v.q == 1 && s.v.rank == 0 && s.v.stages == s.m;
+    split_band(L, stepwise_exact ? 1 : s.m, &mainb, &band);
     int launches = 0;
     SweepCall sc;
     sc.src = src;
