@@ -104,7 +104,7 @@ constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 #define SB_S2_PB 2
 #endif
 #ifndef SB_S2_NSLOT
-#define SB_S2_NSLOT 3
+#define SB_S2_NSLOT 5
 #endif
 #ifndef SB_S2_MINB
 #define SB_S2_MINB 1
