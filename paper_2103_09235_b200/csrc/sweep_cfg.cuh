@@ -70,7 +70,7 @@ constexpr int vxm2() { return (SHAPE == STENCIL_BOX ? Q * RR >= 2 : Q * RR >= SB
 #define SB_2D_NSLOTH 6
 #endif
 #ifndef SB_2D_NSLOT_PLC
-#define SB_2D_NSLOT_PLC 4
+#define SB_2D_NSLOT_PLC 3
 #endif
 // Window periods of at most 5 planes (Q <= 2) use one-period TMA slots (PB = NW,
 // branch-free phase loop; measured +7% on C3 m=2, +14% on C2 m=4 in 2 passes);
@@ -113,6 +113,9 @@ constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 // 64x32 tile with 3 one-plane slots, 1 CTA/SM (measured 346 vs 318 GStencil/s
 // in one gpurun call; the same change costs 14% on the 7-tap star, which keeps
 // the defaults).
+#ifndef SB_B1_NSLOT
+#define SB_B1_NSLOT 3
+#endif
 template <int SHAPE, int Q, int S, int RR>
 constexpr bool box1_3d() { return SHAPE == STENCIL_BOX && Q == 1 && S == 1 && RR == 1; }
 // two on-chip box steps (C5 m=2)
@@ -139,7 +142,7 @@ using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32,
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : box1_3d<SHAPE, Q, S, RR>() ? 4
                                                     : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_VY : SB_3D_VY),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : SB_3D_PB),
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : box1_3d<SHAPE, Q, S, RR>() ? 3
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_NSLOT
                                                        : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NSLOT : SB_3D_NSLOT), 1,
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_MINB : box1_3d<SHAPE, Q, S, RR>() ? 1
                                                       : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_MINB : SB_3D_MINB),
