@@ -11,10 +11,13 @@ namespace sb {
 #define SB_2D_NTX 256
 #endif
 #ifndef SB_2D_PB
-#define SB_2D_PB 4
+#define SB_2D_PB 8      // 8-row slots x 3 (C2 m=3/4: +1% / +3% over 4 x 6, same-call A/B)
+#endif
+#ifndef SB_2D_PBH
+#define SB_2D_PBH 4
 #endif
 #ifndef SB_2D_NSLOT
-#define SB_2D_NSLOT 6
+#define SB_2D_NSLOT 3
 #endif
 #ifndef SB_3D_NTY
 #define SB_3D_NTY 8
@@ -83,7 +86,7 @@ template <int Q, int RR = 1>
 constexpr bool plc2() { return 2 * Q * RR + 1 <= SB_PLC_MAXNW; }
 template <typename T, int SHAPE, int Q, int S, int RR = 1>
 using Cfg2 = Cfg<T, 2, SHAPE, RR, Q, S, (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NTXH : SB_2D_NTX), 1, 1,
-                 (plc2<Q, RR>() ? 0 : SB_2D_PB),
+                 (plc2<Q, RR>() ? 0 : vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_PBH : SB_2D_PB),
                  (plc2<Q, RR>() ? SB_2D_NSLOT_PLC : vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NSLOTH : SB_2D_NSLOT),
                  vxm2<SHAPE, Q, RR>(), (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_MINBH : SB_2D_MINB),
                  (vxm2<SHAPE, Q, RR>() > 1 && !plc2<Q, RR>() ? SB_ROT_2DH : SB_ROT_2D), SB_PINC_2D>;
