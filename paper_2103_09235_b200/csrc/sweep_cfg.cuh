@@ -119,6 +119,9 @@ constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 #ifndef SB_B1_NSLOT
 #define SB_B1_NSLOT 3
 #endif
+#ifndef SB_B1_PB
+#define SB_B1_PB 1
+#endif
 template <int SHAPE, int Q, int S, int RR>
 constexpr bool box1_3d() { return SHAPE == STENCIL_BOX && Q == 1 && S == 1 && RR == 1; }
 // two on-chip box steps (C5 m=2)
@@ -144,7 +147,7 @@ using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32,
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_NTY : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NTY : SB_3D_NTY),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : box1_3d<SHAPE, Q, S, RR>() ? 4
                                                     : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_VY : SB_3D_VY),
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : SB_3D_PB),
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_PB : SB_3D_PB),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_NSLOT
                                                        : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NSLOT : SB_3D_NSLOT), 1,
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_MINB : box1_3d<SHAPE, Q, S, RR>() ? 1
