@@ -73,7 +73,7 @@ constexpr int vxm2() { return (SHAPE == STENCIL_BOX ? Q * RR >= 2 : Q * RR >= SB
 #define SB_2D_NSLOTH 6
 #endif
 #ifndef SB_2D_NSLOT_PLC
-#define SB_2D_NSLOT_PLC 3
+#define SB_2D_NSLOT_PLC 2   // one-period slots: 2 (C2 m=2 740 vs 701 with 3, C3 m=2 equal; 4: C3 -3%)
 #endif
 // Window periods of at most 5 planes (Q <= 2) use one-period TMA slots (PB = NW,
 // branch-free phase loop; measured +7% on C3 m=2, +14% on C2 m=4 in 2 passes);
