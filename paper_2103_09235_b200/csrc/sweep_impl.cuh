@@ -308,8 +308,8 @@ struct Consumer {
 //
 // Work is distributed by rows (fixed axis-0/axis-1 coordinates): a warp takes
 // 32/LX rows at a time, LX = the smallest power of two >= the row length (at
-// most 32), so thin x-face blocks keep the warp busy and there is one integer
-// division per row, not per cell.  The taps are unrolled at compile time in
+// most 32), so thin x-face blocks keep the warp busy and there is one
+// multiply-high (row / n1) per row, not per cell.  The taps are unrolled at compile time in
 // canonical order (R4) with shared-memory offsets o0*S0 + o1*S1 + o2.
 template <class C, class F>
 __device__ __forceinline__ void band_rows(int n0, int n1, int n2, int tid, int nthr, F&& f) {
@@ -319,10 +319,13 @@ __device__ __forceinline__ void band_rows(int n0, int n1, int n2, int tid, int n
     const int LX = 1 << lg, RPW = 32 >> lg;
     const int lx = lane & (LX - 1), lr = lane >> lg;
     const int rows = n0 * n1;
+    // row / n1 as a multiply-high by ceil(2^32 / n1): exact while rows * n1 < 2^32
+    const unsigned mg = n1 > 1 ? (unsigned)((0x100000000ull + (unsigned)n1 - 1) / (unsigned)n1) : 0u;
     for (int rb = warp * RPW; rb < rows; rb += nwarp * RPW) {
         const int row = rb + lr;
         if (row >= rows) continue;
-        const int c1 = row % n1, c0 = row / n1;
+        const int c0 = n1 > 1 ? (int)__umulhi((unsigned)row, mg) : row;
+        const int c1 = row - c0 * n1;
         f(c0, c1, lx, LX);
     }
 }
@@ -332,11 +335,14 @@ struct PeerStores {
     int h, lo_on, hi_on;
 };
 
+// Geometry of one band block: output box [olo, ohi), loaded box ilo + [0, ie),
+// clo/chi = the loaded box was clipped at a FIXED face (the ring is its edge).
+struct BandGeo {
+    int olo[3], ohi[3], ilo[3], ie[3], clo[3], chi[3];
+};
+
 template <class C>
-__device__ __forceinline__ void band_block(const BandDesc<typename C::T>& bd, const DevGeom& g,
-                                           const typename C::T* __restrict__ src, typename C::T* __restrict__ dst,
-                                           int blk_id, typename C::T* smem, int tid, int nthr, const PeerStores& ps) {
-    using T = typename C::T;
+__device__ __forceinline__ BandGeo band_geo(const BandDesc<typename C::T>& bd, const DevGeom& g, int blk_id) {
     constexpr int RR = C::RR;
     constexpr bool used[3] = {true, C::ND == 3, true};
     int b = 0;
@@ -347,62 +353,104 @@ __device__ __forceinline__ void band_block(const BandDesc<typename C::T>& bd, co
     t /= bd.nblk[b][2];
     bi[1] = t % bd.nblk[b][1];
     bi[0] = t / bd.nblk[b][1];
-    int olo[3], ohi[3], ilo[3], ie[3], clo[3], chi[3];
+    BandGeo q;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-        olo[a] = bd.lo[b][a] + bi[a] * bd.blk[b][a];
-        ohi[a] = min(olo[a] + bd.blk[b][a], bd.hi[b][a]);
+        q.olo[a] = bd.lo[b][a] + bi[a] * bd.blk[b][a];
+        q.ohi[a] = min(q.olo[a] + bd.blk[b][a], bd.hi[b][a]);
         const int H = used[a] ? bd.m * RR : 0;
-        int lo = olo[a] - H, hi = ohi[a] + H;
-        clo[a] = used[a] && g.phys_lo[a] && lo < -RR;
-        chi[a] = used[a] && g.phys_hi[a] && hi > g.n[a] + RR;
-        if (clo[a]) lo = -RR;
-        if (chi[a]) hi = g.n[a] + RR;
-        ilo[a] = lo;
-        ie[a] = hi - lo;
+        int lo = q.olo[a] - H, hi = q.ohi[a] + H;
+        q.clo[a] = used[a] && g.phys_lo[a] && lo < -RR;
+        q.chi[a] = used[a] && g.phys_hi[a] && hi > g.n[a] + RR;
+        if (q.clo[a]) lo = -RR;
+        if (q.chi[a]) hi = g.n[a] + RR;
+        q.ilo[a] = lo;
+        q.ie[a] = hi - lo;
     }
-    const int S1 = ie[2], S0 = ie[1] * ie[2];
-    T* cur = smem;
-    T* nxt = smem + ie[0] * S0;
+    return q;
+}
+
+// Issue the block's loads (cp.async / LDGSTS: global -> shared without a
+// register round trip, so every thread keeps many loads in flight; cells
+// outside the allocation are zero-filled, src-size 0).  The caller commits and
+// waits.
+template <class C>
+__device__ __forceinline__ void band_load(const BandGeo& q, const DevGeom& g, const typename C::T* __restrict__ src,
+                                          typename C::T* buf, int tid, int nthr) {
+    using T = typename C::T;
+    const int S1 = q.ie[2], S0 = q.ie[1] * q.ie[2];
     const long long s0 = g.stride0, s1 = g.stride1;
-    band_rows<C>(ie[0], ie[1], ie[2], tid, nthr, [&](int c0, int c1, int lx, int LX) {
-        const long long a0 = g.origin[0] + ilo[0] + c0, a1 = g.origin[1] + ilo[1] + c1;
+    band_rows<C>(q.ie[0], q.ie[1], q.ie[2], tid, nthr, [&](int c0, int c1, int lx, int LX) {
+        const long long a0 = g.origin[0] + q.ilo[0] + c0, a1 = g.origin[1] + q.ilo[1] + c1;
         const bool rowin = a0 >= 0 && a0 < g.ext[0] && a1 >= 0 && a1 < g.ext[1];
-        const T* gp = src + a0 * s0 + a1 * s1 + g.origin[2] + ilo[2];
-        T* sp = cur + c0 * S0 + c1 * S1;
-        // cp.async (LDGSTS): global -> shared without a register round trip, so
-        // every thread keeps many loads in flight (the band is latency-bound);
-        // cells outside the allocation are zero-filled (src-size 0).
-        for (int c2 = lx; c2 < ie[2]; c2 += LX) {
-            const long long a2 = g.origin[2] + ilo[2] + c2;
-            const bool ok = rowin && a2 >= 0 && a2 < g.ext[2];
+        const int b2 = (int)g.origin[2] + q.ilo[2];   // allocation x of c2 = 0
+        const T* gp = src + a0 * s0 + a1 * s1 + b2;
+        T* sp = buf + c0 * S0 + c1 * S1;
+        const int v0 = rowin ? max(0, -b2) : q.ie[2], v1 = min(q.ie[2], g.ext[2] - b2);
+        for (int c2 = lx; c2 < q.ie[2]; c2 += LX) {
+            const bool ok = c2 >= v0 && c2 < v1;
             ptx::cp_async<sizeof(T)>(sp + c2, ok ? gp + c2 : src, ok);
         }
     });
-    ptx::cp_async_wait_all();
-    __syncthreads();
+}
+
+// The block's m single steps on the shrinking region (ring cells frozen) and
+// its store; the loads into buf must be complete and visible (caller's
+// wait + __syncthreads).  Ends with __syncthreads: buf is free afterwards.
+template <class C>
+__device__ __forceinline__ void band_finish(const BandDesc<typename C::T>& bd, const BandGeo& q, const DevGeom& g,
+                                            typename C::T* __restrict__ dst, typename C::T* buf, int tid, int nthr,
+                                            const PeerStores& ps) {
+    using T = typename C::T;
+    constexpr int RR = C::RR;
+    constexpr bool used[3] = {true, C::ND == 3, true};
+    const int S1 = q.ie[2], S0 = q.ie[1] * q.ie[2];
+    T* cur = buf;
+    T* nxt = buf + q.ie[0] * S0;
+    const long long s0 = g.stride0, s1 = g.stride1;
     for (int s = 1; s <= bd.m; ++s) {
         int rlo[3], re[3];
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
             const int sh = used[a] ? s * RR : 0;
-            rlo[a] = clo[a] ? 0 : sh;
-            re[a] = ie[a] - rlo[a] - (chi[a] ? 0 : sh);
+            rlo[a] = q.clo[a] ? 0 : sh;
+            re[a] = q.ie[a] - rlo[a] - (q.chi[a] ? 0 : sh);
         }
         band_rows<C>(re[0], re[1], re[2], tid, nthr, [&](int d0, int d1, int lx, int LX) {
             const int c0 = d0 + rlo[0], c1 = d1 + rlo[1];
-            const int q0 = ilo[0] + c0, q1 = ilo[1] + c1;
+            const int q0 = q.ilo[0] + c0, q1 = q.ilo[1] + c1;
             const bool rowring = (q0 < 0 && g.phys_lo[0]) || (q0 >= g.n[0] && g.phys_hi[0]) ||
                                  (used[1] && ((q1 < 0 && g.phys_lo[1]) || (q1 >= g.n[1] && g.phys_hi[1])));
             const int lrow = c0 * S0 + c1 * S1;
-            for (int d2 = lx; d2 < re[2]; d2 += LX) {
-                const int c2 = d2 + rlo[2], q2 = ilo[2] + c2;
-                const int li = lrow + c2;
-                T acc;
-                if (rowring || (q2 < 0 && g.phys_lo[2]) || (q2 >= g.n[2] && g.phys_hi[2])) {
-                    acc = cur[li];
-                } else {
-                    acc = T(0);
+            auto ring2 = [&](int c2) {
+                const int q2 = q.ilo[2] + c2;
+                return rowring || (q2 < 0 && g.phys_lo[2]) || (q2 >= g.n[2] && g.phys_hi[2]);
+            };
+            // one cell: the original taps in canonical order (R4)
+            auto cell = [&](int li) {
+                T acc = T(0);
+                int j = 0;
+#pragma unroll
+                for (int o0 = -RR; o0 <= RR; ++o0)
+#pragma unroll
+                    for (int o1 = (used[1] ? -RR : 0); o1 <= (used[1] ? RR : 0); ++o1)
+#pragma unroll
+                        for (int o2 = -RR; o2 <= RR; ++o2) {
+                            if (!in_support<C::SHAPE, RR, 1>(o0, o1, o2)) continue;
+                            acc = fmaT(bd.w[j], cur[li + o0 * S0 + o1 * S1 + o2], acc);
+                            ++j;
+                        }
+                return acc;
+            };
+            // two cells per lane in flight: independent FMA chains (the band is
+            // latency-bound), each cell's sum in the same order as alone
+            for (int d2 = lx; d2 < re[2]; d2 += 2 * LX) {
+                const int ca = d2 + rlo[2], cb = ca + LX;
+                const bool hb = d2 + LX < re[2];
+                const bool ra = ring2(ca), rb = !hb || ring2(cb);
+                const int la = lrow + ca, lb = la + LX;
+                if (!ra && !rb) {
+                    T aa = T(0), ab = T(0);
                     int j = 0;
 #pragma unroll
                     for (int o0 = -RR; o0 <= RR; ++o0)
@@ -411,11 +459,17 @@ __device__ __forceinline__ void band_block(const BandDesc<typename C::T>& bd, co
 #pragma unroll
                             for (int o2 = -RR; o2 <= RR; ++o2) {
                                 if (!in_support<C::SHAPE, RR, 1>(o0, o1, o2)) continue;
-                                acc = fmaT(bd.w[j], cur[li + o0 * S0 + o1 * S1 + o2], acc);
+                                const int o = o0 * S0 + o1 * S1 + o2;
+                                aa = fmaT(bd.w[j], cur[la + o], aa);
+                                ab = fmaT(bd.w[j], cur[lb + o], ab);
                                 ++j;
                             }
+                    nxt[la] = aa;
+                    nxt[lb] = ab;
+                } else {
+                    nxt[la] = ra ? cur[la] : cell(la);
+                    if (hb) nxt[lb] = ring2(cb) ? cur[lb] : cell(lb);
                 }
-                nxt[li] = acc;
             }
         });
         __syncthreads();
@@ -423,20 +477,20 @@ __device__ __forceinline__ void band_block(const BandDesc<typename C::T>& bd, co
         cur = nxt;
         nxt = tmp;
     }
-    const int oe0 = ohi[0] - olo[0], oe1 = ohi[1] - olo[1], oe2 = ohi[2] - olo[2];
+    const int oe0 = q.ohi[0] - q.olo[0], oe1 = q.ohi[1] - q.olo[1], oe2 = q.ohi[2] - q.olo[2];
     band_rows<C>(oe0, oe1, oe2, tid, nthr, [&](int d0, int d1, int lx, int LX) {
-        const T* sp = cur + (olo[0] - ilo[0] + d0) * S0 + (olo[1] - ilo[1] + d1) * S1 + (olo[2] - ilo[2]);
-        T* gp = dst + (g.origin[0] + olo[0] + d0) * s0 + (g.origin[1] + olo[1] + d1) * s1 + g.origin[2] + olo[2];
+        const T* sp = cur + (q.olo[0] - q.ilo[0] + d0) * S0 + (q.olo[1] - q.ilo[1] + d1) * S1 + (q.olo[2] - q.ilo[2]);
+        T* gp = dst + (g.origin[0] + q.olo[0] + d0) * s0 + (g.origin[1] + q.olo[1] + d1) * s1 + g.origin[2] + q.olo[2];
         for (int d2 = lx; d2 < oe2; d2 += LX) gp[d2] = sp[d2];
         if (ps.h > 0) {   // fused halo exchange (NEXT-2)
-            const int z = olo[0] + d0;
+            const int z = q.olo[0] + d0;
             if (ps.lo_on && z < ps.h) {
-                T* q = reinterpret_cast<T*>(reinterpret_cast<char*>(gp) + ps.dlo);
-                for (int d2 = lx; d2 < oe2; d2 += LX) q[d2] = sp[d2];
+                T* t = reinterpret_cast<T*>(reinterpret_cast<char*>(gp) + ps.dlo);
+                for (int d2 = lx; d2 < oe2; d2 += LX) t[d2] = sp[d2];
             }
             if (ps.hi_on && z >= g.n[0] - ps.h) {
-                T* q = reinterpret_cast<T*>(reinterpret_cast<char*>(gp) + ps.dhi);
-                for (int d2 = lx; d2 < oe2; d2 += LX) q[d2] = sp[d2];
+                T* t = reinterpret_cast<T*>(reinterpret_cast<char*>(gp) + ps.dhi);
+                for (int d2 = lx; d2 < oe2; d2 += LX) t[d2] = sp[d2];
             }
         }
     });
@@ -942,14 +996,18 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
     // ================================================================ band (tail filler)
     if (p.band.nblk_total > 0) {
         __shared__ int s_blk;
+        const PeerStores ps{p.peer_dlo, p.peer_dhi, p.peer_h, p.peer_lo_on, p.peer_hi_on};
         __syncthreads();
         for (;;) {
             if (threadIdx.x == 0) s_blk = (int)atomicAdd(&p.sc.ctr[(p.sc.epoch & 1) * 2 + 1], 1u);
             __syncthreads();
             const int blk = s_blk;
             if (blk >= p.band.nblk_total) break;
-            band_block<C>(p.band, p.g, p.src, p.dst, blk, slots, threadIdx.x, C::NTHREADS,
-                          PeerStores{p.peer_dlo, p.peer_dhi, p.peer_h, p.peer_lo_on, p.peer_hi_on});
+            const BandGeo q = band_geo<C>(p.band, p.g, blk);
+            band_load<C>(q, p.g, p.src, slots, threadIdx.x, C::NTHREADS);
+            ptx::cp_async_wait_all();
+            __syncthreads();
+            band_finish<C>(p.band, q, p.g, p.dst, slots, threadIdx.x, C::NTHREADS, ps);
         }
     }
 }
