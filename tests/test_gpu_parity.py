@@ -356,3 +356,17 @@ def test_uncompiled_fold_is_unsupported():
     from paper_2103_09235_b200 import StencilError
     with pytest.raises(StencilError):
         run_case((19, 37, 75), "box", "f64", 7, 4, 0)      # 3D fold 4: not compiled
+
+
+# The exact boundary band (K-G3) under stress: band boxes cut into
+# several ragged blocks along every axis (the 64-cell block cap and the shared-memory
+# fit), bands thicker than half an axis (the main region empty along it), and domains
+# that are all band.
+@pytest.mark.parametrize("dims,shape,dtype,m,T", [
+    ((3, 70, 130), "star", "f64", 2, 5), ((70, 3, 130), "box", "f32", 2, 4),
+    ((67, 66, 3), "star", "f64", 2, 4), ((2, 40, 41), "box", "f64", 2, 6),
+    ((5, 5, 5), "star", "f32", 2, 7), ((4, 600), "star", "f64", 4, 9),
+    ((600, 5), "box", "f32", 4, 8), ((130, 300), "box", "f64", 3, 7)])
+def test_band_geometry(dims, shape, dtype, m, T):
+    got, ref, u0, _ = run_case(dims, shape, dtype, T, m, 1)
+    assert np.max(np.abs(got - ref)) <= TOL[dtype] * np.max(np.abs(u0))
