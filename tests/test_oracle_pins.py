@@ -283,3 +283,112 @@ def test_generator_counter_form_is_sequential_splitmix64():
     u = synth.u0_frame((5, 6), 1, 2)
     assert u.shape == (7, 8)
     assert np.array_equal(u.ravel(), synth.uniform(2, np.arange(56)))
+
+
+# ---------------------------------------------------------------- radius > 1
+# The same four pins at r = 2 (and r = 3, 4 in 1D): the 1D5P workload of
+# Table 1 and the radius-2 stencils of NEXT-4.  The ring is r
+# wide; every tap reaches at most r cells, so the affine operator, the exact
+# rational run and the Fourier closed form are built the same way as for r = 1.
+
+@pytest.mark.parametrize("dims,r,shape", [((9,), 2, oracle.STAR), ((11,), 3, oracle.STAR),
+                                          ((12,), 4, oracle.STAR), ((6, 7), 2, oracle.STAR),
+                                          ((5, 6), 2, oracle.BOX), ((4, 5, 6), 2, oracle.STAR),
+                                          ((3, 4, 5), 2, oracle.BOX)])
+def test_matrix_power_fixed_radius(dims, r, shape):
+    offs = oracle.taps(len(dims), r, shape)
+    assert len(offs) == (2 * len(dims) * r + 1 if shape == oracle.STAR else (2 * r + 1) ** len(dims))
+    w = RNG.uniform(0.1, 1.0, len(offs))
+    w = w / w.sum()
+    P = tuple(n + 2 * r for n in dims)
+    u0 = RNG.uniform(-1, 1, P)
+    T = 7
+    M, pts = _affine_operator(dims, r, offs, w, u0)
+    M = np.array(M)
+    v = np.array([u0[tuple(c + r for c in p)] for p in pts] + [1.0])
+    vT = np.linalg.matrix_power(M, T) @ v
+    got = oracle.run(dims, r, offs, w, u0, T)
+    for i, p in enumerate(pts):
+        assert abs(got[tuple(c + r for c in p)] - vT[i]) <= 1e-13
+    mask = np.ones(P, bool)
+    mask[tuple(slice(r, r + n) for n in dims)] = False
+    assert np.array_equal(got[mask], u0[mask])
+
+
+@pytest.mark.parametrize("dims,r,shape,T", [((10,), 2, oracle.STAR, 6), ((6, 5), 2, oracle.STAR, 4),
+                                            ((5, 5), 2, oracle.BOX, 3), ((3, 4, 4), 2, oracle.STAR, 3)])
+def test_exact_dyadic_fractions_radius(dims, r, shape, T):
+    """Bitwise equality with exact rational arithmetic at r = 2 (dyadic inputs)."""
+    offs = oracle.taps(len(dims), r, shape)
+    w = synth.dyadic_weights(len(offs), seed=9)
+    P = tuple(n + 2 * r for n in dims)
+    u0 = synth.dyadic_field(P, seed=13)
+    Mf, pts = _affine_operator(dims, r, offs, [Fraction(x) for x in w],
+                               np.vectorize(Fraction, otypes=[object])(u0))
+    v = [Fraction(u0[tuple(c + r for c in p)]) for p in pts] + [Fraction(1)]
+    for _ in range(T):
+        v = [sum((Mf[i][j] * v[j] for j in range(len(v)) if Mf[i][j] != 0), Fraction(0))
+             for i in range(len(v))]
+    got = oracle.run(dims, r, offs, w, u0, T)
+    for i, p in enumerate(pts):
+        assert Fraction(got[tuple(c + r for c in p)]) == v[i]
+
+
+@pytest.mark.parametrize("dims,r,shape", [((20,), 2, oracle.STAR), ((24,), 3, oracle.STAR),
+                                          ((12, 14), 2, oracle.STAR), ((10, 12), 2, oracle.BOX),
+                                          ((8, 10, 12), 2, oracle.STAR), ((6, 8, 10), 2, oracle.BOX)])
+def test_fourier_mode_periodic_radius(dims, r, shape):
+    """Periodic Fourier mode at r > 1: the r-wide wrapped ring must carry the
+    interior cells r away, or sigma(theta)^T fails."""
+    nd = len(dims)
+    offs = oracle.taps(nd, r, shape)
+    w = RNG.uniform(0.2, 1.0, len(offs))
+    w = w / w.sum()
+    k = [1 + (a % 2) for a in range(nd)]
+    theta = np.array([2 * math.pi * k[a] / dims[a] for a in range(nd)])
+    P = tuple(n + 2 * r for n in dims)
+    grids = np.meshgrid(*[np.arange(n) - r for n in P], indexing="ij")
+    phase = sum(theta[a] * grids[a] for a in range(nd))
+    T = 8
+    uc = oracle.run(dims, r, offs, w, np.cos(phase), T, oracle.PERIODIC)
+    us = oracle.run(dims, r, offs, w, np.sin(phase), T, oracle.PERIODIC)
+    sigma = sum(wj * np.exp(1j * float(np.dot(theta, o))) for o, wj in zip(offs, w))
+    expect = sigma ** T * np.exp(1j * phase)
+    assert np.max(np.abs(uc - expect.real)) < 1e-13
+    assert np.max(np.abs(us - expect.imag)) < 1e-13
+
+
+@pytest.mark.parametrize("nd,r,shape,bc", [(1, 2, oracle.STAR, oracle.FIXED), (1, 4, oracle.STAR, oracle.PERIODIC),
+                                           (2, 2, oracle.STAR, oracle.FIXED), (2, 2, oracle.BOX, oracle.PERIODIC),
+                                           (3, 2, oracle.STAR, oracle.FIXED), (3, 2, oracle.BOX, oracle.FIXED)])
+def test_constant_field_radius(nd, r, shape, bc):
+    dims = [9, 7, 6][:nd]
+    offs = oracle.taps(nd, r, shape)
+    w = synth.weights(len(offs), 3)
+    c = 0.7
+    P = tuple(n + 2 * r for n in dims)
+    T = 20
+    got = oracle.run(dims, r, offs, w, np.full(P, c), T, bc)
+    assert np.max(np.abs(got - c)) <= T * (len(offs) + 1) * 2.0 ** -53 * c * 2
+
+
+def test_radius2_fold_equals_steps_away_from_boundary():
+    """R2/R8 at r = 2: one application of lambda^(2) (reach 2r) equals two steps
+    at distance >= (m-1) r = 2 from every FIXED face, and differs at distance 0."""
+    r, m, dims = 2, 2, [14, 13]
+    offs = oracle.taps(2, r, oracle.STAR)
+    w = RNG.uniform(0.1, 1.0, len(offs))
+    w = w / w.sum()
+    P = tuple(n + 2 * r for n in dims)
+    u0 = RNG.uniform(0, 1, P)
+    step = oracle.run(dims, r, offs, w, u0, m)
+    lam = oracle.fold_ref(oracle.dense_from_taps(2, r, offs, w), m)
+    assert lam.shape == (4 * r + 1,) * 2
+    fold = _apply_dense_once(u0, lam, dims, r, m)
+    for p in _interior_index(dims):
+        q = tuple(c + r for c in p)
+        dist = min(min(p[a], dims[a] - 1 - p[a]) for a in range(2))
+        if dist >= (m - 1) * r:
+            assert abs(step[q] - fold[q]) < 1e-14
+        elif dist == 0:
+            assert not (abs(step[q] - fold[q]) < 1e-14)
