@@ -230,6 +230,107 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- ours
+def quick_measure(key, rank, world, dev, exchange, steps=5):
+    """One config at N GPUs (weak scaling along axis 0 for N > 1): every fold_m
+    of the config for 2 steps, then the best one for `steps` steps with the
+    dominant kernel's launches timed by CUDA events (live roofline)."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2103_09235_b200 import Plan
+    from paper_2103_09235_b200.dist import make_comm, make_peer_comm
+    cfg = CONFIGS[key]
+    dims = list(cfg["dims"])
+    if world > 1:
+        dims[0] *= world
+    nd = len(dims)
+    k = {(1, "star"): 3, (2, "star"): 5, (2, "box"): 9, (3, "star"): 7, (3, "box"): 27}[(nd, cfg["shape"])]
+    plan = Plan(dims, 1, cfg["shape"], config_weights(cfg, k), cfg["dtype"])
+    T = cfg["T"]
+    ms = list(cfg["ms"])
+    halo = max(ms)
+    comm = None
+    if world > 1:
+        L = plan.layout_dist(rank, world, halo)
+        a, b, ws = (plan.empty(layout=L) for _ in range(3))
+        plan.fill_random_dist(rank, world, halo, a, synth.DEFAULT_SEED_U)
+        comm = make_peer_comm(b, ws, dev) if exchange == "peer" else make_comm(dev)
+    else:
+        L = plan.layout
+        a, b, ws = plan.empty(), plan.empty(), plan.empty()
+        plan.fill_random(a, synth.DEFAULT_SEED_U)
+    stream = torch.cuda.current_stream()
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if 3 * L.bytes < 126e6 else None
+
+    def step(m):
+        if world > 1:
+            plan.run_dist(comm, a, b, T, m, halo, ws)
+        else:
+            plan.run(a, b, T, m, ws)
+
+    def allmax(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def timed(m, n):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(n):
+            if flush is not None:
+                flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            step(m)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            tot += e0.elapsed_time(e1)
+        if world > 1:
+            dist.barrier()
+        return allmax(tot / n)
+
+    points = 1
+    for n in dims:
+        points *= n
+    variants = []
+    for m in ms:
+        step(m)
+        t_ms = timed(m, 2)
+        variants.append({"fold_m": m, "ms_per_step": t_ms, "gstencil_s": points * T / (t_ms * 1e-3) / 1e9})
+    m = min(variants, key=lambda v: v["ms_per_step"])["fold_m"]
+    step(m)
+    plan.timing_reset()
+    plan.set_timing(True)
+    t_ms = timed(m, steps)
+    plan.set_timing(False)
+    km = plan.timing(0)
+    plan.timing_reset()
+    if comm is not None:
+        comm.close()
+    peaks, _ = measured_peaks()
+    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    avg = km["ms"] / max(1, km["launches"])
+    ach = km["bytes"] / max(1, km["launches"]) / (avg * 1e-3) / 1e9 if avg > 0 else None
+    fpk = 148 * (64 if cfg["dtype"] == "f64" else 128) * float(peaks.get("sm_max_mhz", 1965.0)) * 1e6 / 1e12
+    fach = km["fmas"] / max(1, km["launches"]) / (avg * 1e-3) / 1e12 if avg > 0 else None
+    out = {"workload": cfg["name"] + (" x%d rows (slab per GPU)" % world if world > 1 else ""),
+           "dims": dims, "T": T, "n_gpus": world, "scaling": "weak" if world > 1 else None,
+           "best_m": m, "value": points * T / (t_ms * 1e-3) / 1e9, "unit": UNIT, "ms_per_step": t_ms,
+           "steps": steps,
+           "roofline": {"bound": "hbm", "achieved": ach, "peak": hbm, "unit": "GB/s",
+                        "frac": ach / hbm if ach else None, "avg_launch_ms": avg, "launches": km["launches"],
+                        "fma_frac": fach / fpk if fach else None},
+           "variants": variants}
+    del a, b, ws, plan
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -396,34 +497,18 @@ def run_ours(args):
     barrier()
     pipelined = world == 1
     if pipelined:
-        # Steps overlap on the GPU's copy engines: the H2D of step k+1 and the D2H of
-        # step k-1 run while step k computes (two device buffer sets, one copy stream
-        # each way; the compute stays on one stream, every step still copies its whole
-        # input in and its whole result out).
+        # The library's batch entry point with HOST buffers (stencil_run_host_batch):
+        # every problem copies its whole input frame in and its whole result out;
+        # the library pipelines the copies of neighbouring problems on its own
+        # copy streams against the compute (two device buffer sets).
         sets = [(a, b, ws), (plan.empty(), plan.empty(), plan.empty())]
         outs_h = [out_host, plan.empty("cpu", layout=L, pin_memory=True)]
-        s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
-        ev = {k: [torch.cuda.Event() for _ in range(2)] for k in ("in", "comp", "out")}
+        plan.run_host_batch([in_host] * 2, outs_h, T, m, sets, args.stages)   # warm the pipeline objects
+        torch.cuda.synchronize()
         x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        x0.record(s_in)
-        for k in range(ke):
-            j = k % 2
-            din, dout, dws = sets[j]
-            if k >= 2:
-                s_in.wait_event(ev["comp"][j])          # step k-2 finished reading din
-            with torch.cuda.stream(s_in):
-                din.copy_(in_host, non_blocking=True)
-            ev["in"][j].record(s_in)
-            stream.wait_event(ev["in"][j])
-            if k >= 2:
-                stream.wait_event(ev["out"][j])         # step k-2's result left dout
-            plan.run(din, dout, T, m, dws, args.stages)
-            ev["comp"][j].record(stream)
-            s_out.wait_event(ev["comp"][j])
-            with torch.cuda.stream(s_out):
-                outs_h[j].copy_(dout, non_blocking=True)
-            ev["out"][j].record(s_out)
-        x1.record(s_out)
+        x0.record(stream)
+        plan.run_host_batch([in_host] * ke, [outs_h[k % 2] for k in range(ke)], T, m, sets, args.stages)
+        x1.record(stream)
         torch.cuda.synchronize()
         e2e_ms = x0.elapsed_time(x1) / ke
     else:
@@ -436,6 +521,16 @@ def run_ours(args):
         barrier()
         e2e_ms = allmax(x0.elapsed_time(x1) / ke)
 
+    # --- the other configs (extra keys; the headline stays args.config): every
+    # fold_m of each, best one timed with live kernel events.  At N > 1 only the
+    # weak-scaling config C5 (768x768x(384 N), BASELINE configs[4]) is added.
+    sets = outs_h = None
+    torch.cuda.empty_cache()
+    extra = {}
+    if not args.headline_only:
+        keys = [k for k in ("c1", "c2", "c3", "c4", "c5") if k != args.config] if world == 1 else ["c5"]
+        for key in keys:
+            extra[key] = quick_measure(key, rank, world, dev, args.exchange, steps=5)
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -488,12 +583,14 @@ def run_ours(args):
             "e2e": {"value": points * T / (e2e_ms * 1e-3) / 1e9, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms, "steps": ke,
                     "pipelined": pipelined,
-                    "how": ("pinned host -> device copy of the whole input frame, Plan.run, device -> pinned host "
-                            "copy of the whole result, every step; copies of neighbouring steps overlap the "
-                            "compute on the copy engines" if pipelined else
-                            "stencil_run_host / run_dist with H2D and D2H copies, every step, one stream")},
+                    "how": ("one stencil_run_host_batch call over the timed steps: per step a pinned host -> "
+                            "device copy of the whole input frame, stencil_run, a device -> pinned host copy of "
+                            "the whole result; the library overlaps the copies of neighbouring steps with the "
+                            "compute on its copy streams" if pipelined else
+                            "stencil_run_dist with H2D and D2H copies, every step, one stream")},
             "roofline": roof,
             "clocks": cl,
+            "configs": extra,
             "variants": variants, "variants_note": variants_note}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args.config)
@@ -516,9 +613,21 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--exchange", choices=["nccl", "peer"], default="nccl",
                     help="N>1 halo exchange: NCCL send/recv (default) or fused peer stores (NEXT-2)")
+    ap.add_argument("--headline-only", action="store_true",
+                    help="skip the per-config extra measurements (configs key)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # launched as `python bench.py --gpus N`: start the N ranks ourselves
+        # (one process per GPU, torchrun on this node); rank 0 prints the line
+        import socket
+        with socket.socket() as so:
+            so.bind(("127.0.0.1", 0))
+            port = so.getsockname()[1]
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(args.gpus),
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
     return run_ours(args)
 
 

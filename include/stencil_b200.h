@@ -36,6 +36,13 @@
  *    for its sweep schedule, so the runs of ONE plan must be ordered (one
  *    stream, or streams synchronised by the caller); different plans run
  *    concurrently.  A plan is not thread-safe for concurrent calls.
+ *  - CUDA graphs: runs may be captured (cudaStreamBeginCapture) and replayed.
+ *    A captured 2D/3D sweep zeroes the plan's schedule scratch before and
+ *    after its kernel (memset nodes), so replays do not depend on the launch
+ *    order.  Run the same call once eagerly before capturing it (the scratch
+ *    may have to grow, which is not allowed while capturing: EUNSUPPORTED).
+ *    A graph is valid while its plan lives and the scratch does not grow
+ *    (a later eager call on a larger domain reallocates it).
  *  - Axes are listed slowest first (z, y, x); x has unit stride.
  */
 #ifndef STENCIL_B200_H
@@ -58,7 +65,8 @@ typedef enum {
     STENCIL_EUNSUPPORTED = -2,  /* valid request this build does not compile (e.g. PERIODIC dist runs, fold_m*r too large) */
     STENCIL_ECUDA = -3,         /* CUDA runtime/driver error (message in stencil_last_error) */
     STENCIL_ENCCL = -4,         /* NCCL error or NCCL library not loadable */
-    STENCIL_ENOMEM = -5         /* host allocation failed */
+    STENCIL_ENOMEM = -5,        /* host allocation failed */
+    STENCIL_ETIMEOUT = -6       /* stencil_comm_wait: the stream did not drain in time (comm aborted) */
 } stencil_status;
 
 typedef enum { STENCIL_STAR = 0, STENCIL_BOX = 1 } stencil_shape;
@@ -231,6 +239,38 @@ int stencil_run_host(stencil_plan plan, const void *in_host, void *out_host, int
                      int fold_m, int stages, void *dev_in, void *dev_out, void *workspace,
                      void *stream);
 
+/*
+ * A batch of `nbatch` independent problems from HOST memory (the e2e path of
+ * the measurement): problem k copies in_hosts[k] -> device, runs
+ * stencil_run_ex(T, fold_m, stages) and copies the result -> out_hosts[k].
+ * Pipelined: the library's two internal copy streams overlap problem k's
+ * H2D and problem k-2's D2H with problem k-1's run on `stream`, using two
+ * device buffer sets alternately.  dev = 6 device pointers {in0, out0, ws0,
+ * in1, out1, ws1} of the plan layout (set 1 unused when nbatch == 1; ws may
+ * be NULL when a run needs no workspace).  Host buffers: plan layout, pinned
+ * (page-locked) for the copies to be asynchronous.  Ordered after prior work
+ * on `stream`; `stream` waits for every copy of the batch, so synchronising
+ * it makes all out_hosts valid.  Errors: EINVAL (NULL), as stencil_run_ex, ECUDA.
+ */
+int stencil_run_host_batch(stencil_plan plan, int nbatch, const void *const *in_hosts,
+                           void *const *out_hosts, int64_t T, int fold_m, int stages,
+                           void *const *dev, void *stream);
+
+/*
+ * Dynamic-schedule controls and counters of the 2D/3D sweep (tests and
+ * tuning).  The persistent CTAs claim `chunk`-plane pieces of their own column
+ * segment, then grab never-started segments, then steal the upper half of the
+ * largest remaining segment if it has at least `min_steal` planes
+ * (DESIGN.md §5.1); max_ctas > 0 caps the persistent grid (so CTAs must
+ * grab).  stencil_plan_set_schedule(plan, 0, 0, 0) restores the defaults.
+ * stencil_plan_sched_stats returns the successful grabs and steals
+ * counted by the kernels since the plan's scratch was allocated or last reset
+ * (synchronous device read; reset != 0 zeroes them).
+ * Errors: EINVAL (NULL, negative values), ECUDA.
+ */
+int stencil_plan_set_schedule(stencil_plan plan, int chunk, int min_steal, int max_ctas);
+int stencil_plan_sched_stats(stencil_plan plan, int64_t *grabs, int64_t *steals, int reset);
+
 /* Number of kernel launches the last run on this plan enqueued (host count). */
 int stencil_plan_last_launches(stencil_plan plan, int64_t *launches);
 
@@ -283,9 +323,22 @@ int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void *in_local,
                      void *out_local, int64_t T, int fold_m, int stages, int halo,
                      void *workspace, void *stream);
 
-/* Exchange the ghost planes of a local slab buffer (collective). */
+/* Exchange the ghost planes of a local slab buffer (collective).  NCCL comms
+ * only (a peer comm returns EINVAL: its ghosts are written by the sweep). */
 int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void *buf, int halo,
                           void *stream);
+
+/*
+ * Failure detection.  Wait until `stream` has drained, polling
+ * the NCCL communicator's asynchronous error (ncclCommGetAsyncError) every
+ * 0.2 ms.  On an asynchronous NCCL error the communicator is aborted
+ * (ncclCommAbort) and ENCCL is returned; if the stream has not drained after
+ * timeout_ms (< 0: no limit) the communicator is aborted and ETIMEOUT is
+ * returned.  An aborted comm makes every later run/exchange on it return
+ * ENCCL.  Every NCCL call inside run_dist/halo_exchange is checked and the
+ * async error is also polled before each exchange.  Host-blocking.
+ */
+int stencil_comm_wait(stencil_comm comm, void *stream, int64_t timeout_ms);
 
 /*
  * Fused halo exchange over peer memory (one process per
@@ -296,11 +349,17 @@ int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void *buf, int h
  * stream memory operations on small flag words (cuStreamWriteValue32 after
  * each sweep, cuStreamWaitValue32 before the next: no spinning kernel).
  *   1. stencil_comm_create_peer(&c, rank, nranks, buf0, buf1): buf0/buf1 =
- *      this rank's ping-pong buffers (every run must pass them as out and
- *      workspace, in either order);
+ *      this rank's ping-pong buffers; every run on every rank must pass
+ *      buf0 as `out` and buf1 as `workspace` (a rank stores into the
+ *      neighbour's buffer of the same registered index; EINVAL otherwise);
  *   2. stencil_comm_peer_handles(c, rec): writes 3 * STENCIL_PEER_HANDLE_BYTES;
  *   3. all-gather the records (rank order) and stencil_comm_peer_attach(c, all);
- *   4. stencil_run_dist(plan, c, ...) as with an NCCL comm.
+ *   4. stencil_run_dist(plan, c, ...) as with an NCCL comm.  Every sweep,
+ *      the last one included, stores into the neighbours' ghost planes, so
+ *      after the run out_local's ghosts hold the neighbours' final planes and
+ *      a copy of out_local (ghosts included) is a complete in_local for a
+ *      chained run.  Between runs all ranks must synchronise (stream sync +
+ *      process barrier) before touching their buffers.
  * Errors: EINVAL (NULL, bad rank, buffers not the registered pair), ECUDA
  * (IPC / stream memory operations unavailable or failing).
  */

@@ -43,7 +43,12 @@ SIGNATURES = {
     "stencil_run": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_vp, c_vp]),
     "stencil_run_ex": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp]),
     "stencil_run_host": (c_int, [c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_vp, c_vp, c_vp, c_vp]),
+    "stencil_run_host_batch": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i64, c_int, c_int,
+                                       ctypes.POINTER(c_vp), c_vp]),
     "stencil_plan_last_launches": (c_int, [c_vp, ctypes.POINTER(c_i64)]),
+    "stencil_plan_set_schedule": (c_int, [c_vp, c_int, c_int, c_int]),
+    "stencil_plan_sched_stats": (c_int, [c_vp, ctypes.POINTER(c_i64), ctypes.POINTER(c_i64), c_int]),
+    "stencil_comm_wait": (c_int, [c_vp, c_vp, c_i64]),
     "stencil_plan_set_timing": (c_int, [c_vp, c_int]),
     "stencil_plan_timing": (c_int, [c_vp, c_int, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_i64),
                                     ctypes.POINTER(c_i64), ctypes.POINTER(c_i64)]),
@@ -65,7 +70,7 @@ SIGNATURES = {
 }
 
 STATUS = {0: "STENCIL_OK", -1: "STENCIL_EINVAL", -2: "STENCIL_EUNSUPPORTED", -3: "STENCIL_ECUDA",
-          -4: "STENCIL_ENCCL", -5: "STENCIL_ENOMEM"}
+          -4: "STENCIL_ENCCL", -5: "STENCIL_ENOMEM", -6: "STENCIL_ETIMEOUT"}
 
 
 class StencilError(RuntimeError):

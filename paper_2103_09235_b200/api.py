@@ -198,6 +198,30 @@ class Plan:
         check(self._lib.stencil_run_host(self._h, _ptr(in_host), _ptr(out_host), int(T), int(fold_m), int(stages),
                                          _ptr(dev_in), _ptr(dev_out), _ptr(workspace), _stream(stream)))
 
+    def run_host_batch(self, in_hosts, out_hosts, T: int, fold_m: int, dev_sets, stages: int = 0, stream=None):
+        """nbatch problems from pinned host buffers, H2D / run / D2H pipelined over
+        two device buffer sets dev_sets = [(in, out, ws), (in, out, ws)]
+        (stencil_run_host_batch)."""
+        n = len(in_hosts)
+        if len(out_hosts) != n:
+            raise ValueError("in_hosts and out_hosts differ in length")
+        arr = ctypes.c_void_p * n
+        flat = [_ptr(t) for s in list(dev_sets)[:2] for t in s]
+        flat += [None] * (6 - len(flat))
+        check(self._lib.stencil_run_host_batch(self._h, n, arr(*[_ptr(t) for t in in_hosts]),
+                                               arr(*[_ptr(t) for t in out_hosts]), int(T), int(fold_m), int(stages),
+                                               (ctypes.c_void_p * 6)(*flat), _stream(stream)))
+
+    def set_schedule(self, chunk: int = 0, min_steal: int = 0, max_ctas: int = 0) -> None:
+        """Schedule granularity of the 2D/3D sweep (tests/tuning; 0 = default)."""
+        check(self._lib.stencil_plan_set_schedule(self._h, int(chunk), int(min_steal), int(max_ctas)))
+
+    def sched_stats(self, reset: bool = False):
+        """(grabs, steals) counted by the sweep kernels (stencil_plan_sched_stats)."""
+        g, s = ctypes.c_int64(), ctypes.c_int64()
+        check(self._lib.stencil_plan_sched_stats(self._h, ctypes.byref(g), ctypes.byref(s), 1 if reset else 0))
+        return g.value, s.value
+
     @property
     def last_launches(self) -> int:
         n = ctypes.c_int64()
@@ -265,7 +289,7 @@ class Comm:
     @classmethod
     def peer(cls, rank: int, nranks: int, buf0, buf1) -> "Comm":
         """Fused peer-store exchange (NEXT-2): buf0/buf1 are this rank's
-        ping-pong buffers (every run passes them as out and workspace).  Attach
+        ping-pong buffers (every run passes buf0 as out and buf1 as workspace).  Attach
         the neighbours with attach(all_records) after an all-gather of
         handles() (paper_2103_09235_b200.dist.make_peer_comm does both)."""
         self = cls.__new__(cls)
@@ -289,6 +313,11 @@ class Comm:
         if len(blob) != self.PEER_RECORD * self.nranks:
             raise ValueError("expected %d records of %d bytes" % (self.nranks, self.PEER_RECORD))
         check(self._lib.stencil_comm_peer_attach(self._h, blob))
+
+    def wait(self, stream=None, timeout_ms: int = -1) -> None:
+        """Block until `stream` drains, polling the NCCL async error; abort the
+        comm and raise on an NCCL failure or after timeout_ms (stencil_comm_wait)."""
+        check(self._lib.stencil_comm_wait(self._h, _stream(stream), int(timeout_ms)))
 
     def close(self):
         if getattr(self, "_h", None) is not None and self._h.value:

@@ -25,10 +25,14 @@ static K1Fn<T> k1_pick(int V, int r, int m, bool wrap) {
 // Cells per lane: the smallest of {8, 16, 32} holding the fold radius; the
 // env var STENCIL_1D_V overrides it (tuning).
 int onchip1d_cells_per_lane(int r, int m, bool wrap) {
-    static int forced = [] {
+#ifdef STENCIL_TUNING_BUILD
+    static int forced = [] {   // (tuning builds only)
         const char* e = getenv("STENCIL_1D_V");
         return e ? atoi(e) : 0;
     }();
+#else
+    constexpr int forced = 0;
+#endif
     int v = (r * m <= 8 && !wrap) ? 8 : r * m <= 16 ? 16 : 32;
     if (wrap) return v;
     if (forced == 16 && r * m <= 16) v = 16;   // (tuning) the only other compiled choice

@@ -70,6 +70,12 @@ struct Plan {
     void* sched = nullptr;
     int64_t sched_words = 0;
     unsigned int epoch = 0;
+    // stencil_run_host_batch: internal copy streams + pipeline events (lazy)
+    void* h2d_stream = nullptr;
+    void* d2h_stream = nullptr;
+    void* pipe_ev[7] = {};   // start, in[2], comp[2], out[2]
+    // schedule granularity override (stencil_plan_set_schedule; 0 = default)
+    int sched_chunk = 0, sched_min_steal = 0, sched_max_ctas = 0;
 };
 
 const std::vector<double>& folded(Plan* p, int q);   // cached lambda^(q)

@@ -349,6 +349,10 @@ int stencil_plan_destroy(stencil_plan plan) {
         }
         for (void* e : p->event_pool) cudaEventDestroy((cudaEvent_t)e);
         if (p->sched) cudaFree(p->sched);
+        for (void* e : p->pipe_ev)
+            if (e) cudaEventDestroy((cudaEvent_t)e);
+        if (p->h2d_stream) cudaStreamDestroy((cudaStream_t)p->h2d_stream);
+        if (p->d2h_stream) cudaStreamDestroy((cudaStream_t)p->d2h_stream);
         for (auto& kv : p->lowrank) delete kv.second;
     }
     delete p;

@@ -9,6 +9,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -60,6 +62,12 @@ static int ensure_device(Plan* p) {
     cudaError_t e = cudaGetDevice(&dev);
     if (e != cudaSuccess) return cuda_error(e, "cudaGetDevice");
     if (p->device != dev || p->sm_count <= 0) {
+        if (p->device >= 0 && p->device != dev && p->sched) {
+            // the schedule scratch lives on the previous device
+            cudaFree(p->sched);
+            p->sched = nullptr;
+            p->sched_words = 0;
+        }
         int sms = 0;
         e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         if (e != cudaSuccess) return cuda_error(e, "cudaDeviceGetAttribute");
@@ -141,9 +149,13 @@ static int enqueue_sweep(Plan* p, const Layout3& L, const void* src, void* dst, 
         sc.coef = &folded(p, s.v.q);
     }
     sc.stream = stream;
+#ifdef STENCIL_TUNING_BUILD
     // STENCIL_DEBUG_NO_BAND=1 drops the band (WRONG results near FIXED faces):
-    // only to measure what the band costs (tools/, never in tests or bench)
+    // only in tuning builds (tools/tunebuild.py), to measure what the band costs
     static const bool no_band = getenv("STENCIL_DEBUG_NO_BAND") != nullptr;
+#else
+    constexpr bool no_band = false;
+#endif
     if (s.m > 1 && !no_band) {
         for (const Box& b : band) {
             Box c = clip0(b, z0, z1);
@@ -234,10 +246,14 @@ static int run_1d(Plan* p, const Layout3& L, const void* in, void* out, int64_t 
     // cells as outputs, i.e. a halo H = TB*r <= 8*V; a multiple of m
     // (STENCIL_1D_HMAX overrides the 8*V halo bound: tuning)
     const int V = onchip1d_cells_per_lane(p->r, m, L.wrap);
-    static const int64_t hforce = [] {
+#ifdef STENCIL_TUNING_BUILD
+    static const int64_t hforce = [] {   // (tuning builds only)
         const char* e = getenv("STENCIL_1D_HMAX");
         return e ? (int64_t)atoll(e) : (int64_t)0;
     }();
+#else
+    constexpr int64_t hforce = 0;
+#endif
     const int64_t hmax = std::min<int64_t>(hforce > 0 ? hforce : 8 * V, 16 * V - 1) / p->r;
     int64_t cap = std::max<int64_t>(m, hmax / m * m);
     int64_t nl = (T + cap - 1) / cap;
@@ -363,6 +379,8 @@ struct NcclApi {
     ncclResult_t (*GroupStart)() = nullptr;
     ncclResult_t (*GroupEnd)() = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
+    ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
     bool ok = false;
     std::string why;
 };
@@ -385,6 +403,8 @@ static NcclApi& nccl() {
         LOAD("ncclGroupStart", GroupStart);
         LOAD("ncclGroupEnd", GroupEnd);
         LOAD("ncclGetErrorString", GetErrorString);
+        LOAD("ncclCommGetAsyncError", CommGetAsyncError);
+        LOAD("ncclCommAbort", CommAbort);
 #undef LOAD
         api.ok = true;
     });
@@ -439,6 +459,7 @@ struct stencil_comm_s {
     uint32_t* flags = nullptr;
     uint32_t* nflag[2] = {nullptr, nullptr};   // neighbour's flag slot this rank writes
     uint32_t epoch = 0;
+    bool failed = false;   // NCCL comm aborted (async error or stencil_comm_wait timeout)
 };
 
 namespace sb {
@@ -509,10 +530,12 @@ static int run_dist_peer(sb::Plan* p, stencil_comm_s* c, const sb::Layout3& L, c
                          void* ws, int64_t n, int64_t nf, int fold_m, sb::Variant v, int mr, sb::Variant vr, int64_t hx,
                          void* stream) {
     using namespace sb;
-    if (!((out_local == c->buf[0] && (n < 2 || ws == c->buf[1])) ||
-          (out_local == c->buf[1] && (n < 2 || ws == c->buf[0]))))
-        return set_error(STENCIL_EINVAL, "peer comm: out/workspace must be the buffers the comm was created with");
-    const int bo = out_local == c->buf[0] ? 0 : 1;   // registered index of `out`
+    // One fixed order on every rank: a rank's peer stores go into
+    // the neighbour's buffer of the same REGISTERED index, so all ranks must
+    // use buf0 as `out` and buf1 as the workspace.
+    if (!(out_local == c->buf[0] && (n < 2 || ws == c->buf[1])))
+        return set_error(STENCIL_EINVAL, "peer comm: out must be buf0 and workspace buf1 (the registered order)");
+    const int bo = 0;   // registered index of `out`
     DrvMemOps& d = drv();
     if (!d.wait32 || !d.write32) return set_error(STENCIL_ECUDA, "cuStreamWaitValue32/WriteValue32 unavailable");
     CUstream cs = (CUstream)stream;
@@ -543,9 +566,12 @@ static int run_dist_peer(sb::Plan* p, stencil_comm_s* c, const sb::Layout3& L, c
             if (has_hi && d.wait32(cs, (CUdeviceptr)(c->flags + 1), want, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
                 return set_error(STENCIL_ECUDA, "cuStreamWaitValue32");
         }
-        const bool xchg = j < n;
-        rc = enqueue_sweep(p, L, src, bufs[di], s, 0, L.n[0], stream, xchg && has_lo ? c->nbuf[0][reg] : nullptr,
-                           xchg && has_hi ? c->nbuf[1][reg] : nullptr, (int)hx);
+        // every sweep stores its boundary planes into the neighbours' ghosts,
+        // the last one included: after the run out_local's ghost planes hold
+        // the neighbours' final planes, so a copy of out_local is a complete
+        // in_local for a chained run (no separate exchange needed)
+        rc = enqueue_sweep(p, L, src, bufs[di], s, 0, L.n[0], stream, has_lo ? c->nbuf[0][reg] : nullptr,
+                           has_hi ? c->nbuf[1][reg] : nullptr, (int)hx);
         if (rc < 0) return rc;
         launches += rc;
         {   // every sweep signals, the last one included (orders the next run)
@@ -589,6 +615,34 @@ int stencil_fill_random_dist(stencil_plan plan, int rank, int nranks, int halo, 
     if (rc) return rc;
     rc = launch_fill(p, buf, &L, seed, stream);
     return rc < 0 ? rc : STENCIL_OK;
+}
+
+int stencil_plan_set_schedule(stencil_plan plan, int chunk, int min_steal, int max_ctas) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || chunk < 0 || min_steal < 0 || max_ctas < 0) return set_error(STENCIL_EINVAL, "bad argument");
+    p->sched_chunk = chunk;
+    p->sched_min_steal = min_steal;
+    p->sched_max_ctas = max_ctas;
+    return STENCIL_OK;
+}
+
+int stencil_plan_sched_stats(stencil_plan plan, int64_t* grabs, int64_t* steals, int reset) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !grabs || !steals) return set_error(STENCIL_EINVAL, "NULL argument");
+    *grabs = 0;
+    *steals = 0;
+    if (!p->sched) return STENCIL_OK;
+    unsigned int* st = reinterpret_cast<unsigned int*>(static_cast<unsigned long long*>(p->sched) + p->sched_words - 4);
+    unsigned int h[2] = {0, 0};
+    cudaError_t e = cudaMemcpy(h, st, sizeof(h), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) return cuda_error(e, "cudaMemcpy(schedule stats)");
+    *grabs = h[0];
+    *steals = h[1];
+    if (reset) {
+        e = cudaMemset(st, 0, sizeof(h));
+        if (e != cudaSuccess) return cuda_error(e, "cudaMemset(schedule stats)");
+    }
+    return STENCIL_OK;
 }
 
 int stencil_plan_set_timing(stencil_plan plan, int enable) {
@@ -657,6 +711,67 @@ int stencil_run_host(stencil_plan plan, const void* in_host, void* out_host, int
     if (rc) return rc;
     e = cudaMemcpyAsync(out_host, dev_out, L.bytes, cudaMemcpyDeviceToHost, st);
     if (e != cudaSuccess) return cuda_error(e, "cudaMemcpyAsync D2H");
+    return STENCIL_OK;
+}
+
+// A batch of independent problems from host memory, pipelined across the
+// GPU's copy engines: problem k's H2D (copy stream 1) and problem k-2's D2H
+// (copy stream 2) overlap problem k-1's run (the caller's stream), on two
+// device buffer sets used alternately.  Hazards are ordered with events:
+// H2D into set j waits until the run two problems back finished reading it,
+// a run into set j waits until that set's previous result left the device.
+int stencil_run_host_batch(stencil_plan plan, int nbatch, const void* const* in_hosts, void* const* out_hosts,
+                           int64_t T, int fold_m, int stages, void* const* dev, void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || nbatch < 0 || (nbatch > 0 && (!in_hosts || !out_hosts || !dev)))
+        return set_error(STENCIL_EINVAL, "NULL argument");
+    if (nbatch == 0) return STENCIL_OK;
+    const int sets = nbatch >= 2 ? 2 : 1;
+    for (int j = 0; j < sets; ++j)
+        if (!dev[3 * j] || !dev[3 * j + 1]) return set_error(STENCIL_EINVAL, "NULL device buffer");
+    for (int k = 0; k < nbatch; ++k)
+        if (!in_hosts[k] || !out_hosts[k]) return set_error(STENCIL_EINVAL, "NULL host buffer");
+    cudaError_t e = cudaSuccess;
+    if (!p->h2d_stream) e = cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&p->h2d_stream), cudaStreamNonBlocking);
+    if (e == cudaSuccess && !p->d2h_stream)
+        e = cudaStreamCreateWithFlags(reinterpret_cast<cudaStream_t*>(&p->d2h_stream), cudaStreamNonBlocking);
+    for (void*& ev : p->pipe_ev)
+        if (e == cudaSuccess && !ev) e = cudaEventCreateWithFlags(reinterpret_cast<cudaEvent_t*>(&ev), cudaEventDisableTiming);
+    if (e != cudaSuccess) return cuda_error(e, "run_host_batch streams/events");
+    Layout3 L = make_layout(p, 0, 1, 0);
+    cudaStream_t st = (cudaStream_t)stream, si = (cudaStream_t)p->h2d_stream, so = (cudaStream_t)p->d2h_stream;
+    cudaEvent_t* ev = reinterpret_cast<cudaEvent_t*>(p->pipe_ev);
+    cudaEvent_t e_start = ev[0], *e_in = ev + 1, *e_comp = ev + 3, *e_out = ev + 5;
+    int64_t launches = 0;
+#define CK(x, what)                                   \
+    do {                                              \
+        cudaError_t _e = (x);                         \
+        if (_e != cudaSuccess) return cuda_error(_e, what); \
+    } while (0)
+    CK(cudaEventRecord(e_start, st), "cudaEventRecord");
+    CK(cudaStreamWaitEvent(si, e_start, 0), "cudaStreamWaitEvent");
+    CK(cudaStreamWaitEvent(so, e_start, 0), "cudaStreamWaitEvent");
+    for (int k = 0; k < nbatch; ++k) {
+        const int j = k % sets;
+        void* din = dev[3 * j];
+        void* dout = dev[3 * j + 1];
+        void* dws = dev[3 * j + 2];
+        if (k >= sets) CK(cudaStreamWaitEvent(si, e_comp[j], 0), "cudaStreamWaitEvent");
+        CK(cudaMemcpyAsync(din, in_hosts[k], L.bytes, cudaMemcpyHostToDevice, si), "cudaMemcpyAsync H2D");
+        CK(cudaEventRecord(e_in[j], si), "cudaEventRecord");
+        CK(cudaStreamWaitEvent(st, e_in[j], 0), "cudaStreamWaitEvent");
+        if (k >= sets) CK(cudaStreamWaitEvent(st, e_out[j], 0), "cudaStreamWaitEvent");
+        int rc = run_single(p, din, dout, T, fold_m, stages, dws, stream);
+        if (rc) return rc;
+        launches += p->last_launches;
+        CK(cudaEventRecord(e_comp[j], st), "cudaEventRecord");
+        CK(cudaStreamWaitEvent(so, e_comp[j], 0), "cudaStreamWaitEvent");
+        CK(cudaMemcpyAsync(out_hosts[k], dout, L.bytes, cudaMemcpyDeviceToHost, so), "cudaMemcpyAsync D2H");
+        CK(cudaEventRecord(e_out[j], so), "cudaEventRecord");
+    }
+    for (int j = 0; j < sets; ++j) CK(cudaStreamWaitEvent(st, e_out[j], 0), "cudaStreamWaitEvent");
+#undef CK
+    p->last_launches = launches;
     return STENCIL_OK;
 }
 
@@ -788,7 +903,29 @@ int stencil_comm_destroy(stencil_comm comm) {
     return STENCIL_OK;
 }
 
+// NCCL failure detection: the communicator's asynchronous error
+// (a peer died, a network/NVLink fault) is polled before every exchange and
+// by stencil_comm_wait; every call's return code is checked.
+static int nccl_async_check(stencil_comm_s* c) {
+    NcclApi& a = nccl();
+    if (!a.ok) return set_error(STENCIL_ENCCL, a.why);
+    if (!c->comm) return set_error(STENCIL_EINVAL, "not an NCCL comm");
+    if (c->failed) return set_error(STENCIL_ENCCL, "communicator aborted after an earlier failure");
+    ncclResult_t ar = ncclSuccess;
+    ncclResult_t r = a.CommGetAsyncError(c->comm, &ar);
+    if (r != ncclSuccess) return nccl_error(r, "ncclCommGetAsyncError");
+    if (ar != ncclSuccess && ar != ncclInProgress) {
+        c->failed = true;
+        a.CommAbort(c->comm);
+        c->comm = nullptr;
+        return nccl_error(ar, "NCCL asynchronous error (communicator aborted)");
+    }
+    return STENCIL_OK;
+}
+
 static int nccl_exchange(Plan* p, stencil_comm_s* c, const Layout3& L, void* buf, int64_t hx, cudaStream_t st) {
+    int rc = nccl_async_check(c);
+    if (rc) return rc;
     NcclApi& a = nccl();
     const ncclDataType_t dt = p->dtype == STENCIL_F64 ? ncclDouble : ncclFloat;
     const size_t cnt = (size_t)hx * L.stride[0];
@@ -797,15 +934,21 @@ static int nccl_exchange(Plan* p, stencil_comm_s* c, const Layout3& L, void* buf
     auto plane = [&](int64_t z) { return base + (size_t)(L.origin[0] + z) * pb; };
     ncclResult_t r = a.GroupStart();
     if (r != ncclSuccess) return nccl_error(r, "ncclGroupStart");
+    ncclResult_t first = ncclSuccess;
+    const char* what = nullptr;
+    auto chk = [&](ncclResult_t x, const char* w) {
+        if (x != ncclSuccess && first == ncclSuccess) { first = x; what = w; }
+    };
     if (c->rank > 0) {
-        a.Send(plane(0), cnt, dt, c->rank - 1, c->comm, st);
-        a.Recv(plane(-hx), cnt, dt, c->rank - 1, c->comm, st);
+        chk(a.Send(plane(0), cnt, dt, c->rank - 1, c->comm, st), "ncclSend(lower)");
+        chk(a.Recv(plane(-hx), cnt, dt, c->rank - 1, c->comm, st), "ncclRecv(lower)");
     }
     if (c->rank < c->nranks - 1) {
-        a.Send(plane(L.n[0] - hx), cnt, dt, c->rank + 1, c->comm, st);
-        a.Recv(plane(L.n[0]), cnt, dt, c->rank + 1, c->comm, st);
+        chk(a.Send(plane(L.n[0] - hx), cnt, dt, c->rank + 1, c->comm, st), "ncclSend(upper)");
+        chk(a.Recv(plane(L.n[0]), cnt, dt, c->rank + 1, c->comm, st), "ncclRecv(upper)");
     }
-    r = a.GroupEnd();
+    r = a.GroupEnd();   // always close the group, even after a failed call
+    if (first != ncclSuccess) return nccl_error(first, what);
     if (r != ncclSuccess) return nccl_error(r, "ncclGroupEnd");
     return STENCIL_OK;
 }
@@ -816,8 +959,38 @@ int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void* buf, int h
     Layout3 L;
     int rc = dist_layout_check(p, comm->rank, comm->nranks, halo, 1, &L);
     if (rc) return rc;
+    if (comm->peer)
+        return set_error(STENCIL_EINVAL, "peer comm: ghost planes are written by the sweep kernel; "
+                                         "stencil_halo_exchange needs an NCCL comm");
     if (comm->nranks == 1) return STENCIL_OK;
     return nccl_exchange(p, comm, L, buf, halo, (cudaStream_t)stream);
+}
+
+int stencil_comm_wait(stencil_comm comm, void* stream, int64_t timeout_ms) {
+    if (!comm) return set_error(STENCIL_EINVAL, "NULL argument");
+    cudaStream_t st = (cudaStream_t)stream;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        cudaError_t e = cudaStreamQuery(st);
+        if (e == cudaSuccess) break;
+        if (e != cudaErrorNotReady) return cuda_error(e, "cudaStreamQuery");
+        if (!comm->peer) {
+            int rc = nccl_async_check(comm);
+            if (rc) return rc;
+        }
+        const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(std::chrono::steady_clock::now() - t0).count();
+        if (timeout_ms >= 0 && ms > timeout_ms) {
+            if (!comm->peer && comm->comm) {   // a hung collective: abort so the stream can drain
+                comm->failed = true;
+                nccl().CommAbort(comm->comm);
+                comm->comm = nullptr;
+            }
+            return set_error(STENCIL_ETIMEOUT, "stencil_comm_wait: timed out after " + std::to_string(ms) + " ms");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+    if (!comm->peer) return nccl_async_check(comm);
+    return STENCIL_OK;
 }
 
 int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local, void* out_local, int64_t T,
@@ -852,6 +1025,8 @@ int stencil_run_dist(stencil_plan plan, stencil_comm comm, const void* in_local,
     const int64_t hx = (int64_t)fold_m * p->r;
     if (comm->peer)
         return run_dist_peer(p, comm, L, in_local, out_local, workspace, n, nf, fold_m, v, mr, vr, hx, stream);
+    rc = nccl_async_check(comm);
+    if (rc) return rc;
     int launches = 0;
     rc = launch_ring_copy(p, in_local, out_local, &L, stream);
     if (rc < 0) return rc;
@@ -951,10 +1126,9 @@ int stencil_run_dist_emulated(stencil_plan plan, int nranks, const void* const* 
             for (int g = 0; g < nranks; ++g) {
                 void* bufs[2] = {out_locals[g], workspaces ? workspaces[g] : nullptr};
                 const void* src = j == 1 ? in_locals[g] : bufs[(n - j + 1) % 2];
-                const bool xchg = j < n;
                 rc = enqueue_sweep(p, Ls[g], src, dsts[g], s, 0, Ls[g].n[0], stream,
-                                   xchg && g > 0 ? dsts[g - 1] : nullptr,
-                                   xchg && g < nranks - 1 ? dsts[g + 1] : nullptr, (int)hx);
+                                   g > 0 ? dsts[g - 1] : nullptr, g < nranks - 1 ? dsts[g + 1] : nullptr,
+                                   (int)hx);
                 if (rc < 0) return rc;
                 launches += rc;
             }

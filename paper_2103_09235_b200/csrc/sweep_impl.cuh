@@ -678,6 +678,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
                 }
                 ok = __shfl_sync(0xffffffffu, ok, 0);
                 if (ok) {
+                    if (lane == 0) atomicAdd(&sc.stats[1], 1u);
                     *vseg = best;
                     *a = __shfl_sync(0xffffffffu, ra, 0);
                     *b = __shfl_sync(0xffffffffu, rb, 0);
@@ -692,6 +693,7 @@ __global__ void __launch_bounds__(C::NTHREADS, C::MINB)
             if (lane == 0) v = (int)atomicAdd(&sc.ctr[(sc.epoch & 1) * 2 + 0], 1u) + (int)gridDim.x;
             v = __shfl_sync(0xffffffffu, v, 0);
             *s = v;
+            if (lane == 0 && v < sc.nseg) atomicAdd(&sc.stats[0], 1u);
             return v < sc.nseg;
         };
         if (lane == 0) ptx::prefetch_tmap(&tmap);
@@ -1062,20 +1064,26 @@ static int make_tmap(const Layout3& L, const void* base, CUtensorMap* map) {
     return STENCIL_OK;
 }
 
+// Occupancy and the >48 KB dynamic shared-memory opt-in are per device (the
+// attribute belongs to the current context), so both are kept per device id.
 template <class C>
 static int occupancy() {
-    static int occ = -1;
-    static std::once_flag once;
-    std::call_once(once, [] {
+    constexpr int MAXDEV = 64;
+    static int occ[MAXDEV] = {};
+    static std::mutex mu;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= MAXDEV) dev = 0;
+    std::lock_guard<std::mutex> g(mu);
+    if (occ[dev] <= 0) {
         if (C::SMEM > 48 * 1024)
             cudaFuncSetAttribute(sweep_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM);
         int o = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o, sweep_kernel<C>, C::NTHREADS, C::SMEM) !=
             cudaSuccess)
             o = 1;
-        occ = std::max(1, o);
-    });
-    return occ;
+        occ[dev] = std::max(1, o);
+    }
+    return occ[dev];
 }
 
 // Cut the band boxes into blocks whose two shared-memory buffers fit in the
@@ -1138,6 +1146,11 @@ static int plan_band(Plan* p, const SweepCall& c, BandDesc<T>* bd, size_t smem_c
     return STENCIL_OK;
 }
 
+static inline bool captured_now(cudaStream_t st) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    return cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusActive;
+}
+
 template <class C>
 static int launch_cfg(Plan* p, const SweepCall& c) {
     using T = typename C::T;
@@ -1183,6 +1196,9 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
         const int ntx = (int)((b.hi[2] - x0 + C::WOX - 1) / C::WOX);
         const int nty = C::ND == 3 ? (int)((b.hi[1] - b.lo[1] + C::WOY - 1) / C::WOY) : 1;
         const int64_t zlen = b.hi[0] - b.lo[0];
+        // segment words pack plane bounds in 24-bit fields (seg_pack)
+        if (b.hi[0] >= (int64_t(1) << 24) || zlen >= (int64_t(1) << 24))
+            return set_error(STENCIL_EUNSUPPORTED, "axis-0 extent >= 2^24 planes");
         const int64_t cols = (int64_t)ntx * nty;
         // initial segments: about one resident wave of CTAs, split by volume.  When
         // there are already at least as many columns as SMs, columns are not split:
@@ -1218,37 +1234,73 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
         int rc = make_tmap<C>(L, c.src, &map);
         if (rc) return rc;
     }
-    // dynamic-schedule scratch + epoch (advanced only for a launch that happens)
+    // dynamic-schedule scratch + epoch (advanced only for a launch that happens).
+    // Layout (64-bit words): [0, nseg) segment words | ... | stats (2 words:
+    // grabs, steals, 2 spare u32) | counters (2 words: [parity][grab, band]).
+    cudaStream_t cst = (cudaStream_t)c.stream;
     if (p->sched_words < nseg + 4) {
+        if (captured_now(cst))
+            return set_error(STENCIL_EUNSUPPORTED, "schedule scratch must grow: run this call once before capturing it");
         if (p->sched) cudaFree(p->sched);
         p->sched = nullptr;
         int64_t words = std::max<int64_t>(nseg + 4, 8192);
         cudaError_t e = cudaMalloc(&p->sched, words * 8);
         if (e != cudaSuccess) return cuda_error(e, "cudaMalloc(schedule scratch)");
-        e = cudaMemsetAsync(p->sched, 0, words * 8, (cudaStream_t)c.stream);
+        e = cudaMemsetAsync(p->sched, 0, words * 8, cst);
         if (e != cudaSuccess) return cuda_error(e, "cudaMemsetAsync");
         p->sched_words = words;
-        p->epoch = 0;
-    }
-    p->epoch = (p->epoch + 1) & 0xFFFFu;
-    if (p->epoch == 0) {
-        cudaMemsetAsync(p->sched, 0, p->sched_words * 8, (cudaStream_t)c.stream);
         p->epoch = 1;
     }
-    prm.sc.seg = static_cast<unsigned long long*>(p->sched);
-    prm.sc.ctr = reinterpret_cast<unsigned int*>(static_cast<unsigned long long*>(p->sched) + p->sched_words - 2);
-    prm.sc.epoch = p->epoch;
+    unsigned long long* sw = static_cast<unsigned long long*>(p->sched);
+    // CUDA graph capture: a captured launch cannot rely on the
+    // epoch tags and counter parity left by the launch before it in replay
+    // order, so it runs with the reserved epoch 1 on a freshly zeroed schedule
+    // and zeroes it again afterwards (restoring the state every eager launch
+    // expects: stale tags, zero counters).  Eager epochs skip 0 and 1.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(cst, &cap) != cudaSuccess) return cuda_error(cudaGetLastError(), "cudaStreamIsCapturing");
+    const bool captured = cap == cudaStreamCaptureStatusActive;
+    auto zero_sched = [&]() -> int {
+        cudaError_t e = cudaMemsetAsync(sw, 0, (size_t)nseg * 8, cst);
+        if (e == cudaSuccess) e = cudaMemsetAsync(sw + p->sched_words - 2, 0, 16, cst);
+        return e == cudaSuccess ? STENCIL_OK : cuda_error(e, "cudaMemsetAsync(schedule)");
+    };
+    unsigned epoch;
+    if (captured) {
+        int rc = zero_sched();
+        if (rc) return rc;
+        epoch = 1;
+    } else {
+        p->epoch = (p->epoch + 1) & 0xFFFFu;
+        if (p->epoch < 2) {   // wrapped: stale tags could alias, start clean
+            cudaError_t e = cudaMemsetAsync(sw, 0, (p->sched_words - 4) * 8, cst);
+            if (e == cudaSuccess) e = cudaMemsetAsync(sw + p->sched_words - 2, 0, 16, cst);
+            if (e != cudaSuccess) return cuda_error(e, "cudaMemsetAsync");
+            p->epoch = 2;
+        }
+        epoch = p->epoch;
+    }
+    prm.sc.seg = sw;
+    prm.sc.ctr = reinterpret_cast<unsigned int*>(sw + p->sched_words - 2);
+    prm.sc.stats = reinterpret_cast<unsigned int*>(sw + p->sched_words - 4);
+    prm.sc.epoch = epoch;
     prm.sc.nseg = (int)nseg;
 #ifndef SB_CHUNK
 #define SB_CHUNK 16
 #endif
-    prm.sc.chunk = std::max(2 * C::PB, SB_CHUNK);
-    prm.sc.min_steal = std::max(2 * prm.sc.chunk, 4 * C::H + 8);
+    prm.sc.chunk = std::max(2 * C::PB, p->sched_chunk > 0 ? p->sched_chunk : SB_CHUNK);
+    prm.sc.min_steal = std::max(p->sched_chunk > 0 ? prm.sc.chunk : 2 * prm.sc.chunk,
+                                p->sched_min_steal > 0 ? p->sched_min_steal : 4 * C::H + 8);
     int64_t tiles = std::min<int64_t>(nseg, target);   // persistent: one resident wave
     if (band_blocks > 0) tiles = std::max<int64_t>(tiles, std::min<int64_t>(band_blocks, target));
-    sweep_kernel<C><<<(unsigned)tiles, C::NTHREADS, C::SMEM, (cudaStream_t)c.stream>>>(map, prm);
+    if (p->sched_max_ctas > 0) tiles = std::min<int64_t>(tiles, p->sched_max_ctas);   // (tests: force grabs)
+    sweep_kernel<C><<<(unsigned)tiles, C::NTHREADS, C::SMEM, cst>>>(map, prm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "sweep_kernel launch");
+    if (captured) {
+        int rc = zero_sched();
+        if (rc) return rc;
+    }
     return 1;
 }
 

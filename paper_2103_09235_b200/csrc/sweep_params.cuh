@@ -33,6 +33,7 @@ struct DevBoxes {
 struct DevSched {
     unsigned long long* seg;
     unsigned int* ctr;        // [2 parities][2]: grab counter, band counter (this launch: epoch & 1)
+    unsigned int* stats;      // cumulative: [0] successful grabs, [1] successful steals (tests)
     unsigned int epoch;
     int nseg;
     int chunk;

@@ -1,0 +1,116 @@
+"""Multi-GPU code paths that can run on ONE GPU (the pool gives one per call).
+
+* The NCCL path end to end with a 1-rank communicator: stencil_comm_unique_id
+  -> stencil_comm_create -> stencil_run_dist -> stencil_comm_wait
+  (ncclCommGetAsyncError polling) -> destroy; equal to stencil_run bitwise.
+* The fused peer-store exchange (NEXT-2) across TWO PROCESSES on the same
+  GPU: real CUDA IPC handles exchanged through torch.distributed (gloo),
+  cudaIpcOpenMemHandle in the other process, the sweep kernel's peer stores
+  into the other process's allocation, cuStreamWriteValue32 into the peer's
+  flag word and cuStreamWaitValue32 on this rank's own flags.  The ranks are
+  HOST-SERIALISED (one run of one sweep per rank per turn, stream sync and a
+  barrier in between), so every flag wait is already satisfied when it is
+  enqueued: no kernel or stream on this GPU ever waits for work of another
+  process that has not been submitted (B200_PROFILING.md forbids mutually
+  waiting ranks on one GPU).  After K turns the slabs equal a 1-GPU run of
+  K sweeps bitwise.
+"""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.multiprocessing as mp
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _plan(dims, shape, dtype):
+    from paper_2103_09235_b200 import Plan
+    offs = oracle.taps(len(dims), 1, oracle.STAR if shape == "star" else oracle.BOX)
+    return Plan(dims, 1, shape, synth.weights(len(offs), 1), dtype)
+
+
+@pytest.mark.parametrize("dims,shape,dtype,T,m", [((256, 300), "star", "f64", 9, 2),
+                                                  ((40, 64, 96), "box", "f32", 6, 2)])
+def test_nccl_single_rank_run_dist(dims, shape, dtype, T, m):
+    from paper_2103_09235_b200.api import Comm
+    plan = _plan(dims, shape, dtype)
+    uid = Comm.unique_id()
+    assert len(uid) == 128
+    comm = Comm(uid, 0, 1)
+    L = plan.layout_dist(0, 1, m)
+    a, b, ws = plan.empty(layout=L), plan.empty(layout=L), plan.empty(layout=L)
+    plan.fill_random_dist(0, 1, m, a, 2)
+    plan.halo_exchange(comm, a, m)              # no neighbours: a no-op that must succeed
+    plan.run_dist(comm, a, b, T, m, m, ws)
+    comm.wait(timeout_ms=60000)
+    a1, ref, rws = plan.empty(), plan.empty(), plan.empty()
+    plan.fill_random(a1, 2)
+    plan.run(a1, ref, T, m, workspace=rws)
+    torch.cuda.synchronize()
+    assert torch.equal(plan.interior_view(b, L), plan.interior_view(ref))
+    comm.close()
+
+
+def _peer_worker(rank, world, port, outdir, dims, shape, dtype, m, K):
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    from paper_2103_09235_b200.dist import make_peer_comm
+    plan = _plan(dims, shape, dtype)
+    halo = m
+    L = plan.layout_dist(rank, world, halo)
+    a = plan.empty(layout=L)
+    plan.fill_random_dist(rank, world, halo, a, 2)
+    b, ws = plan.empty(layout=L), plan.empty(layout=L)
+    comm = make_peer_comm(b, ws)                # real IPC handles across processes
+    torch.cuda.synchronize()
+    dist.barrier()
+    for _ in range(K):
+        for turn in range(world):
+            if turn == rank:
+                plan.run_dist(comm, a, b, m, m, halo, ws)   # one sweep; peer stores into the neighbours' b
+                torch.cuda.synchronize()
+            dist.barrier()
+        a.copy_(b)                              # out, ghosts included, is the next input
+        torch.cuda.synchronize()
+        dist.barrier()
+    np.save(os.path.join(outdir, "r%d.npy" % rank), plan.interior_view(b, L).double().cpu().numpy())
+    comm.close()
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dims,shape,dtype,m,world", [((64, 300), "star", "f64", 2, 2),
+                                                      ((24, 40, 72), "star", "f64", 2, 2),
+                                                      ((96, 260), "box", "f32", 2, 3)])
+def test_peer_exchange_two_processes_host_serialised(dims, shape, dtype, m, world):
+    K = 4
+    port = 29500 + (os.getpid() % 1000)
+    with tempfile.TemporaryDirectory() as d:
+        ctx = mp.get_context("spawn")
+        procs = [ctx.Process(target=_peer_worker, args=(r, world, port, d, dims, shape, dtype, m, K))
+                 for r in range(world)]
+        for p in procs:
+            p.start()
+        for p in procs:
+            p.join(timeout=300)
+        codes = [p.exitcode for p in procs]
+        for p in procs:
+            if p.is_alive():
+                p.kill()
+        assert codes == [0] * world, codes
+        slabs = [np.load(os.path.join(d, "r%d.npy" % r)) for r in range(world)]
+    plan = _plan(dims, shape, dtype)
+    a, b, ws = plan.empty(), plan.empty(), plan.empty()
+    plan.fill_random(a, 2)
+    plan.run(a, b, K * m, m, workspace=ws)
+    torch.cuda.synchronize()
+    single = plan.interior_view(b).double().cpu().numpy()
+    assert np.array_equal(np.concatenate(slabs, axis=0), single)

@@ -252,7 +252,10 @@ def test_peer_comm_single_rank_api():
     comm.attach([rec])
     plan.run_dist(comm, a, b, 9, 2, 2, ws)
     b2, ws2 = plan.empty(layout=L), plan.empty(layout=L)
-    plan.run_dist(comm, a, ws, 1, 1, 2, b)      # registered pair, swapped roles: allowed
+    with pytest.raises(StencilError):           # registered pair, swapped roles: one fixed order
+        plan.run_dist(comm, a, ws, 1, 1, 2, b)
+    with pytest.raises(StencilError):
+        plan.halo_exchange(comm, b, 2)          # peer comm: ghosts come from the sweep kernel
     with pytest.raises(StencilError):
         plan.run_dist(comm, a, b2, 9, 2, 2, ws2)
     torch.cuda.synchronize()

@@ -2,7 +2,8 @@
 
   python tools/tunebuild.py NAME -DSB_3D_VY=4 -DSB_3D_NTY=4 ...
 
-Recompiles the sweep*.cu sources with the extra defines, links it with the in-tree objects
+Recompiles the sweep*.cu, run.cu and aux.cu sources with the extra defines (and
+STENCIL_TUNING_BUILD, which compiles in the environment tuning knobs), links it with the in-tree objects
 of the other sources and writes tunelibs/lib_NAME.so (load it with
 STENCIL_B200_LIB=... to measure a variant; tunelibs/ is scratch, git-ignored).
 """
@@ -20,7 +21,8 @@ def main():
     B.build()
     out = os.path.join(ROOT, "tunelibs")
     os.makedirs(out, exist_ok=True)
-    tuned = [f for f in B.SOURCES if f.startswith("sweep")]
+    tuned = [f for f in B.SOURCES if f.startswith("sweep") or f in ("run.cu", "aux.cu")]
+    defs = ["-DSTENCIL_TUNING_BUILD"] + defs   # enables the STENCIL_DEBUG_* / STENCIL_1D_* env knobs
     objs = []
     for src in tuned:
         obj = os.path.join(out, "%s_%s.o" % (src[:-3], name))
