@@ -297,6 +297,24 @@ def quick_measure(key, rank, world, dev, exchange, steps=5):
     points = 1
     for n in dims:
         points *= n
+    graphs = {}
+    if nd == 1 and world == 1:
+        # a 1D run is shorter than its launch path: replay a captured graph (as the headline does)
+        for m in ms:
+            step(m)
+            torch.cuda.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                step(m)
+            graphs[m] = g
+        plain_step = step
+
+        def step(m):  # noqa: F811
+            if plan_timing[0]:
+                plain_step(m)
+            else:
+                graphs[m].replay()
+    plan_timing = [False]
     variants = []
     for m in ms:
         step(m)
@@ -305,8 +323,14 @@ def quick_measure(key, rank, world, dev, exchange, steps=5):
     m = min(variants, key=lambda v: v["ms_per_step"])["fold_m"]
     step(m)
     plan.timing_reset()
-    plan.set_timing(True)
-    t_ms = timed(m, steps)
+    if graphs:
+        t_ms = timed(m, steps)       # graph replays; kernel events from a second, eager pass
+        plan_timing[0] = True
+        plan.set_timing(True)
+        timed(m, steps)
+    else:
+        plan.set_timing(True)
+        t_ms = timed(m, steps)
     plan.set_timing(False)
     km = plan.timing(0)
     plan.timing_reset()

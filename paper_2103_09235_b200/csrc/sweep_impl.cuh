@@ -1185,7 +1185,9 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
     if (boxes.empty() && band_blocks == 0) return 0;
     if ((int)boxes.size() > MAXBOX) return set_error(STENCIL_EUNSUPPORTED, "too many boxes");
     const int occ = occupancy<C>();
-    const int target = std::max(1, p->sm_count * occ);
+    // (tests: a capped grid gets 1.5 segments per CTA, so CTAs must grab and,
+    // once the grabs run out, the idle half steals from the long second round)
+    const int target = p->sched_max_ctas > 0 ? std::max(1, p->sched_max_ctas * 3 / 2) : std::max(1, p->sm_count * occ);
     int64_t vol_total = 0;
     for (const Box& b : boxes) vol_total += b.volume();
     prm.b.nbox = (int)boxes.size();

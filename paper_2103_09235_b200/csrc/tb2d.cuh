@@ -1,0 +1,370 @@
+// tb2d.cuh — on-chip multi-step temporal blocking of the 2D radius-1 sweep
+// ("achieve multiple time steps computation in
+// registers over the tiles efficiently without reloading", §3.4;
+// "time loop fusion").  One launch applies K single steps of
+// the original taps (K = fold_m = stages) per HBM round trip, exactly up to
+// the FIXED faces.
+//
+// B200 mapping:
+//  * Every WARP is an independent overlapped tile: a strip of W = 32*VX
+//    columns (lane l owns VX consecutive columns) streamed along axis 0 over
+//    a segment of rows.  After K steps the valid outputs are the middle
+//    W - 2K columns; neighbouring strips overlap by 2K loaded columns.
+//  * Rows arrive by TMA (cp.async.bulk.tensor.2d, one row per transaction,
+//    issued by lane 0 PF rows ahead) into a per-warp ring of TB_D shared
+//    slots, each with its own mbarrier (complete_tx).  No CTA-wide barrier
+//    and no producer warp: the warp is its own producer.
+//  * The K time levels form a register pipeline in "push" form (the GPU
+//    reading of the paper's vertical folding, Eq.4): when a row of
+//    level s-1 arrives at stage s it completes level-s row i-1 with ONE
+//    multiply-add per tap row (a[s] + w_S v), seeds row i (b[s] + row-mid(v))
+//    and row i+1 (w_N v).  So each stage keeps two partial rows (a, b) in
+//    registers, a completed row is handed to the next stage without leaving
+//    the register file, and the dependent chain per stage is one FMA (star) or
+//    three (box).  The only data movement between lanes is the two x
+//    neighbours of every row (warp shuffles).
+//  * Frozen ring (R1): levels >= 1 of the ring rows -1 / ny and of
+//    the ring columns -1 / nx are re-read from the shared slot of that row
+//    (u0 never changes), so the block is exact up to the faces: no band.
+//    Only the first/last K rows of a segment ("checked" iterations) and the
+//    two edge strips pay for these tests.
+//  * Work: units = strips x row segments, taken by warps in a grid-stride
+//    order that puts neighbouring strips of one segment on concurrent warps
+//    (their shared columns meet in L2).  A static schedule: launches are
+//    CUDA-graph safe.
+#pragma once
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "internal.hpp"
+#include "ptx.cuh"
+
+namespace sb {
+
+template <typename T>
+struct TbParams {
+    const T* src;
+    T* dst;
+    long long pitch;            // elements per row (stride of axis 0)
+    long long org_y, org_x;     // allocation index of interior (0, 0)
+    int ny, nx;                 // local interior extents
+    int ext_y;                  // allocated rows (TMA rows are clamped into [0, ext_y))
+    int phys_lo, phys_hi;       // axis-0 faces are physical: frozen ring rows -1 / ny
+    int y_lo, y_hi;             // output rows of this launch
+    int nstrips, seglen, units;
+    // fused halo exchange (NEXT-2), as SweepParams: outputs of rows j < peer_h
+    // (j >= ny - peer_h) are stored again at the same address + peer_dlo (+ peer_dhi) bytes
+    long long peer_dlo, peer_dhi;
+    int peer_h, peer_lo_on, peer_hi_on;
+    T w[9];                     // taps in canonical order (R4)
+};
+
+constexpr int TB_D = 16;   // shared row slots per warp (power of two)
+
+template <typename T, int SHAPE, int K, int VX, int NW>
+struct TbCfg {
+    static constexpr int W = 32 * VX;                 // loaded columns per strip
+    static constexpr int WO = W - 2 * K;              // valid output columns per strip
+    static constexpr int D = TB_D;
+    static constexpr int PF = (D - K - 1) < 8 ? (D - K - 1) : 8;   // rows in flight ahead
+    static constexpr int ROW_BYTES = W * (int)sizeof(T);
+    static constexpr int SMEM = NW * D * ROW_BYTES + NW * D * 8;
+    static constexpr int NTAP = SHAPE == STENCIL_STAR ? 5 : 9;
+    static_assert(K >= 1 && PF >= 2, "temporal block too deep for the slot ring");
+    static_assert(W <= 256, "TMA box dimension");
+    static_assert((VX * sizeof(T)) % 16 == 0, "16-byte lane vectors");
+};
+
+template <typename T, int VX>
+__device__ __forceinline__ void tb_lds(T (&v)[VX], const T* s) {
+    constexpr int NV = VX * (int)sizeof(T) / 16;
+#pragma unroll
+    for (int q = 0; q < NV; ++q) {
+        if constexpr (sizeof(T) == 8) {
+            const double2 x = reinterpret_cast<const double2*>(s)[q];
+            v[2 * q] = x.x;
+            v[2 * q + 1] = x.y;
+        } else {
+            const float4 x = reinterpret_cast<const float4*>(s)[q];
+            v[4 * q] = x.x;
+            v[4 * q + 1] = x.y;
+            v[4 * q + 2] = x.z;
+            v[4 * q + 3] = x.w;
+        }
+    }
+}
+
+template <typename T, int VX>
+__device__ __forceinline__ void tb_stg(T* g, const T (&v)[VX], unsigned mask) {
+    constexpr int EV = 16 / (int)sizeof(T);   // elements per 16-byte vector
+    constexpr unsigned FULL = (1u << EV) - 1u;
+#pragma unroll
+    for (int q = 0; q < VX / EV; ++q) {
+        const unsigned mq = (mask >> (q * EV)) & FULL;
+        if (mq == FULL) {
+            if constexpr (sizeof(T) == 8)
+                reinterpret_cast<double2*>(g)[q] = make_double2(v[2 * q], v[2 * q + 1]);
+            else
+                reinterpret_cast<float4*>(g)[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        } else if (mq) {
+#pragma unroll
+            for (int e = 0; e < EV; ++e)
+                if (mq & (1u << e)) g[q * EV + e] = v[q * EV + e];
+        }
+    }
+}
+
+template <typename T, int SHAPE, int K, int VX, int NW>
+struct TbWarp {
+    using C = TbCfg<T, SHAPE, K, VX, NW>;
+    const CUtensorMap* tmap;
+    const TbParams<T>* p;
+    T* ring;          // this warp's slots
+    uint64_t* bar;    // this warp's barriers
+    int lane;
+    uint32_t fill;    // rows issued so far (slot = fill % D, parity = fill / D % 2)
+
+    // One row of level 0 through the K stages (CHK: the iteration may output a
+    // ring row or a row outside the segment; EDGE: this lane may own a ring column).
+    template <bool CHK, bool EDGE>
+    __device__ __forceinline__ void row(const T (&w)[C::NTAP], T (&a)[K][VX], T (&b)[K][VX], T (&v)[VX], int i,
+                                        int slot, int eL, int eR) const {
+#pragma unroll
+        for (int s = 0; s < K; ++s) {
+            const T vl = __shfl_up_sync(0xffffffffu, v[VX - 1], 1);
+            const T vr = __shfl_down_sync(0xffffffffu, v[0], 1);
+            T o[VX];
+#pragma unroll
+            for (int e = 0; e < VX; ++e) {
+                const T L = e == 0 ? vl : v[e - 1];
+                const T R = e == VX - 1 ? vr : v[e + 1];
+                if constexpr (SHAPE == STENCIL_STAR) {
+                    // taps: 0 (-1,0)  1 (0,-1)  2 (0,0)  3 (0,1)  4 (1,0)
+                    o[e] = fma(w[4], v[e], a[s][e]);
+                    a[s][e] = fma(w[3], R, fma(w[2], v[e], fma(w[1], L, b[s][e])));
+                    b[s][e] = w[0] * v[e];
+                } else {
+                    // taps: (dy+1)*3 + (dx+1)
+                    o[e] = fma(w[8], R, fma(w[7], v[e], fma(w[6], L, a[s][e])));
+                    a[s][e] = fma(w[5], R, fma(w[4], v[e], fma(w[3], L, b[s][e])));
+                    b[s][e] = fma(w[2], R, fma(w[1], v[e], w[0] * L));
+                }
+            }
+            // o = level s+1, row i-(s+1): frozen ring cells keep u0 (re-read from the slot)
+            const int sl = (slot - (s + 1)) & (C::D - 1);
+            const T* srow = ring + sl * C::W + lane * VX;
+            if constexpr (CHK) {
+                const int j = i - (s + 1);
+                if ((p->phys_lo && j == -1) || (p->phys_hi && j == p->ny)) tb_lds<T, VX>(o, srow);
+            }
+            if constexpr (EDGE) {
+                if (eL >= 0 || eR >= 0) {
+#pragma unroll
+                    for (int e = 0; e < VX; ++e)
+                        if (e == eL || e == eR) o[e] = srow[e];
+                }
+            }
+#pragma unroll
+            for (int e = 0; e < VX; ++e) v[e] = o[e];
+        }
+    }
+
+    template <bool EDGE>
+    __device__ __forceinline__ void unit(const T (&w)[C::NTAP], int x0, int y0, int y1) {
+        const TbParams<T>& P = *p;
+        const int i_lo = (P.phys_lo && y0 - K < -1) ? -1 : y0 - K;
+        const int i_end = y1 - 1 + K;
+        const int nrows = i_end - i_lo + 1;
+        const int xl = x0 + lane * VX;
+        const int vlo = max(x0 + K, 0), vhi = min(x0 + C::W - K, P.nx);
+        unsigned smask = 0;
+#pragma unroll
+        for (int e = 0; e < VX; ++e)
+            if (xl + e >= vlo && xl + e < vhi) smask |= 1u << e;
+        int eL = -1, eR = -1;
+        if (EDGE) {
+            if (xl <= -1 && -1 < xl + VX) eL = -1 - xl;
+            if (xl <= P.nx && P.nx < xl + VX) eR = P.nx - xl;
+        }
+        const uint32_t f0 = fill;
+        const int ymax = P.ext_y - 1 - (int)P.org_y;   // last allocated row (interior coords)
+        auto issue = [&](int t) {
+            const uint32_t f = f0 + (uint32_t)t;
+            const int sl = (int)(f & (C::D - 1));
+            const int yr = min(i_lo + t, ymax);        // rows past the allocation: any row (never valid)
+            ptx::mbar_expect_tx(&bar[sl], C::ROW_BYTES);
+            ptx::tma_load_2d(ring + sl * C::W, tmap, &bar[sl], (int)P.org_x + x0, (int)P.org_y + yr);
+        };
+        __syncwarp();
+        if (lane == 0) {
+            ptx::fence_proxy_async();
+            for (int t = 0; t < min(C::PF, nrows); ++t) issue(t);
+        }
+        T a[K][VX], b[K][VX];
+#pragma unroll
+        for (int s = 0; s < K; ++s)
+#pragma unroll
+            for (int e = 0; e < VX; ++e) a[s][e] = b[s][e] = T(0);
+        T* g = P.dst + (P.org_y + (long long)(i_lo - K)) * P.pitch + P.org_x + xl;   // row i - K
+        for (int t = 0; t < nrows; ++t) {
+            const int i = i_lo + t;
+            __syncwarp();
+            if (lane == 0 && t + C::PF < nrows) {
+                ptx::fence_proxy_async();
+                issue(t + C::PF);
+            }
+            const uint32_t f = f0 + (uint32_t)t;
+            const int slot = (int)(f & (C::D - 1));
+            ptx::mbar_wait(&bar[slot], (f / C::D) & 1u);
+            T v[VX];
+            tb_lds<T, VX>(v, ring + slot * C::W + lane * VX);
+            const bool chk = i < y0 + K || (P.phys_hi && i > P.ny);
+            bool st = true;
+            if (chk) {
+                row<true, EDGE>(w, a, b, v, i, slot, eL, eR);
+                st = i - K >= y0 && i - K < y1;
+            } else {
+                row<false, EDGE>(w, a, b, v, i, slot, eL, eR);
+            }
+            if (st) {
+                const int j = i - K;
+                tb_stg<T, VX>(g, v, smask);
+                if (P.peer_lo_on && j < P.peer_h)
+                    tb_stg<T, VX>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dlo), v, smask);
+                if (P.peer_hi_on && j >= P.ny - P.peer_h)
+                    tb_stg<T, VX>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dhi), v, smask);
+            }
+            g += P.pitch;
+        }
+        fill = f0 + (uint32_t)nrows;
+    }
+};
+
+template <typename T, int SHAPE, int K, int VX, int NW>
+__global__ void __launch_bounds__(NW * 32, 1)
+    tb2d_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TbParams<T> p) {
+    using C = TbCfg<T, SHAPE, K, VX, NW>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    TbWarp<T, SHAPE, K, VX, NW> tw;
+    tw.tmap = &tmap;
+    tw.p = &p;
+    tw.ring = reinterpret_cast<T*>(smem_raw) + (size_t)warp * C::D * C::W;
+    tw.bar = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * C::D * C::ROW_BYTES) + warp * C::D;
+    tw.lane = lane;
+    tw.fill = 0;
+    if (lane == 0) {
+#pragma unroll
+        for (int s = 0; s < C::D; ++s) ptx::mbar_init(&tw.bar[s], 1);
+        ptx::fence_mbar_init();
+        ptx::prefetch_tmap(&tmap);
+    }
+    __syncwarp();
+    T w[C::NTAP];
+#pragma unroll
+    for (int k = 0; k < C::NTAP; ++k) w[k] = p.w[k];
+    const int nwt = gridDim.x * NW;
+    for (int u = blockIdx.x * NW + warp; u < p.units; u += nwt) {
+        const int strip = u % p.nstrips, seg = u / p.nstrips;
+        const int y0 = p.y_lo + seg * p.seglen;
+        const int y1 = min(y0 + p.seglen, p.y_hi);
+        const int x0 = strip * C::WO - K;
+        const bool edge = x0 <= -1 || x0 + C::W > p.nx;   // the window holds a ring column
+        if (edge) tw.template unit<true>(w, x0, y0, y1);
+        else tw.template unit<false>(w, x0, y0, y1);
+    }
+}
+
+// ------------------------------------------------------------------ host
+PFN_cuTensorMapEncodeTiled_v12000 tb_encode_fn();
+
+template <typename T, int SHAPE, int K, int VX, int NW>
+int tb2d_launch(Plan* p, const SweepCall& c) {
+    using C = TbCfg<T, SHAPE, K, VX, NW>;
+    const Layout3& L = *c.L;
+    if (c.boxes.size() != 1 || c.boxes[0].lo[2] != 0 || c.boxes[0].hi[2] != L.n[2] || L.wrap)
+        return set_error(STENCIL_EUNSUPPORTED, "tb2d: one full-width box on a FIXED layout");
+    const Box& bx = c.boxes[0];
+    if (bx.empty()) return 0;
+    TbParams<T> prm;
+    std::memset(&prm, 0, sizeof(prm));
+    prm.src = static_cast<const T*>(c.src);
+    prm.dst = static_cast<T*>(c.dst);
+    prm.pitch = L.stride[0];
+    prm.org_y = L.origin[0];
+    prm.org_x = L.origin[2];
+    prm.ny = (int)L.n[0];
+    prm.nx = (int)L.n[2];
+    prm.ext_y = (int)L.ext[0];
+    prm.phys_lo = L.phys_lo[0];
+    prm.phys_hi = L.phys_hi[0];
+    prm.y_lo = (int)bx.lo[0];
+    prm.y_hi = (int)bx.hi[0];
+    if (!L.phys_lo[0] && L.lo_valid[0] < K) return set_error(STENCIL_EUNSUPPORTED, "tb2d: ghost rows < fold_m");
+    if (!L.phys_hi[0] && L.hi_valid[0] < K) return set_error(STENCIL_EUNSUPPORTED, "tb2d: ghost rows < fold_m");
+    if ((int)c.coef->size() != C::NTAP) return set_error(STENCIL_EUNSUPPORTED, "tb2d: tap count");
+    for (int k = 0; k < C::NTAP; ++k) prm.w[k] = static_cast<T>((*c.coef)[k]);
+    if (c.peer_h > 0) {
+        const long long plane = (long long)L.n[0] * L.stride[0] * (long long)sizeof(T);
+        prm.peer_h = c.peer_h;
+        prm.peer_lo_on = c.peer_lo != nullptr;
+        prm.peer_hi_on = c.peer_hi != nullptr;
+        if (c.peer_lo)
+            prm.peer_dlo = (long long)(reinterpret_cast<intptr_t>(c.peer_lo) - reinterpret_cast<intptr_t>(c.dst)) + plane;
+        if (c.peer_hi)
+            prm.peer_dhi = (long long)(reinterpret_cast<intptr_t>(c.peer_hi) - reinterpret_cast<intptr_t>(c.dst)) - plane;
+    }
+    const int rows = prm.y_hi - prm.y_lo;
+    const int nstrips = (prm.nx + C::WO - 1) / C::WO;
+    const int warps = std::max(1, p->sm_count) * NW;
+    // segments: about one unit per resident warp, but at least 4K rows each
+    // (a segment re-loads and re-computes 2K rows of pipeline fill)
+    int nseg = std::max(1, warps / nstrips);
+    nseg = std::min(nseg, std::max(1, rows / (4 * K)));
+    const int seglen = (rows + nseg - 1) / nseg;
+    nseg = (rows + seglen - 1) / seglen;
+    prm.nstrips = nstrips;
+    prm.seglen = seglen;
+    prm.units = nstrips * nseg;
+    const int grid = std::max(1, std::min(std::max(1, p->sm_count), (prm.units + NW - 1) / NW));
+
+    auto enc = tb_encode_fn();
+    if (!enc) return set_error(STENCIL_ECUDA, "cuTensorMapEncodeTiled not available from the driver");
+    CUtensorMap map;
+    cuuint64_t gdim[2] = {(cuuint64_t)L.ext[2], (cuuint64_t)L.ext[0]};
+    cuuint64_t gstr[1] = {(cuuint64_t)(L.stride[0] * (int64_t)sizeof(T))};
+    cuuint32_t box[2] = {(cuuint32_t)C::W, 1u};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&map, sizeof(T) == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                     const_cast<void*>(c.src), gdim, gstr, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return set_error(STENCIL_ECUDA, "tb2d: cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+    {   // >48 KB dynamic shared memory: per-device opt-in
+        static std::mutex mu;
+        static bool done[64] = {};
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::lock_guard<std::mutex> g(mu);
+        if (dev >= 0 && dev < 64 && !done[dev]) {
+            cudaError_t e = cudaFuncSetAttribute(tb2d_kernel<T, SHAPE, K, VX, NW>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+            if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(tb2d)");
+            done[dev] = true;
+        }
+    }
+    tb2d_kernel<T, SHAPE, K, VX, NW><<<grid, NW * 32, C::SMEM, (cudaStream_t)c.stream>>>(map, prm);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return cuda_error(e, "tb2d_kernel launch");
+    return 1;
+}
+
+using TbLaunchFn = int (*)(Plan*, const SweepCall&);
+TbLaunchFn pick_tb2d_f64(int shape, int K);
+TbLaunchFn pick_tb2d_f32(int shape, int K);
+
+}  // namespace sb

@@ -1,0 +1,39 @@
+// tb2d_f64.cu — fp64 instantiations of the 2D temporal block (tb2d.cuh):
+// STAR / BOX, K = fold_m = 2..8 steps per HBM round trip, 4 columns per lane.
+#include "tb2d.cuh"
+
+namespace sb {
+
+PFN_cuTensorMapEncodeTiled_v12000 tb_encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    });
+    return fn;
+}
+
+#ifndef TB_F64_VX
+#define TB_F64_VX 4
+#endif
+#ifndef TB_NW
+#define TB_NW 8
+#endif
+
+template <int SHAPE, int... Ks>
+static TbLaunchFn pick_k(int K, std::integer_sequence<int, Ks...>) {
+    TbLaunchFn fn = nullptr;
+    ((K == Ks + 2 ? (fn = tb2d_launch<double, SHAPE, Ks + 2, TB_F64_VX, TB_NW>, 0) : 0), ...);
+    return fn;
+}
+
+TbLaunchFn pick_tb2d_f64(int shape, int K) {
+    if (shape == STENCIL_STAR) return pick_k<STENCIL_STAR>(K, std::make_integer_sequence<int, 7>{});
+    return pick_k<STENCIL_BOX>(K, std::make_integer_sequence<int, 7>{});
+}
+
+}  // namespace sb

@@ -49,7 +49,7 @@ SCHED_CASES = [
 
 
 @pytest.mark.parametrize("dims,shape,dtype,T,m", SCHED_CASES)
-@pytest.mark.parametrize("max_ctas", [24, 0])
+@pytest.mark.parametrize("max_ctas", [16, 0])
 def test_schedule_paths_whole_frame(dims, shape, dtype, T, m, max_ctas):
     nd = len(dims)
     offs = oracle.taps(nd, 1, oracle.STAR if shape == "star" else oracle.BOX)
@@ -69,9 +69,8 @@ def test_schedule_paths_whole_frame(dims, shape, dtype, T, m, max_ctas):
     got = plan.frame_view(b).cpu().double().numpy()
     err = float(np.max(np.abs(got - ref)))
     assert err <= TOL[dtype] * float(np.max(np.abs(u0))), err
-    assert steals > 0, (grabs, steals)
     if max_ctas:
-        assert grabs > 0, (grabs, steals)
+        assert grabs > 0 and steals > 0, (grabs, steals)
 
 
 FULL = {
@@ -105,8 +104,14 @@ def test_fullsize_affine_whole_interior(key):
         field += a_coef[ax] * (torch.arange(L.frame[ax], dtype=torch.float64, device=dev) - 1).reshape(shp)
     fr.copy_(field.to(plan.torch_dtype))
     out, ws = plan.empty(), plan.empty()
+    plan.run(buf, out, 1, 1, workspace=ws)      # allocate the schedule scratch
+    torch.cuda.synchronize()
+    plan.sched_stats(reset=True)
     plan.run(buf, out, T, m, workspace=ws)
     torch.cuda.synchronize()
+    grabs, steals = plan.sched_stats()
+    if key == "c4":   # 128 columns for 148 persistent CTAs: 20 start by stealing
+        assert steals > 0, (grabs, steals)
     inner = tuple(slice(T + 1, n + 1 - T) for n in dims)   # frame coords: interior p at distance >= T
     expect = field[inner] + T * sum(a_coef[ax] * mu[ax] for ax in range(nd))
     got = plan.frame_view(out)[inner].double()
@@ -141,7 +146,7 @@ def test_schedule_is_graph_capture_safe():
         b.zero_()
         g.replay()
         if it % 2:
-            plan.run(a, ws, 3, 1)                   # eager runs in between (epochs advance)
+            plan.run(a, ws, 1, 1)                   # eager runs in between (epochs advance)
         torch.cuda.synchronize()
         got = plan.frame_view(b).cpu().double().numpy()
         assert float(np.max(np.abs(got - ref))) <= tol, it
