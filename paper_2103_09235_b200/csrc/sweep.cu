@@ -13,12 +13,6 @@ static LaunchFn pick(int dtype, int nd, int shape, int r, int q, int s) {
     return nullptr;
 }
 
-bool sweep_supported(const Plan* p, int q, int s, int rank) {
-    if (rank == 0 && pick_tb(p, q, s, 0, p->boundary == STENCIL_BC_PERIODIC)) return true;
-    if (rank > 0) return s == 1 && p->ndim == 2 && p->r == 1 && pick_cp(p->dtype, q, rank) != nullptr;
-    return pick(p->dtype, p->ndim, p->shape, p->r, q, s) != nullptr;
-}
-
 // The on-chip stepwise block (q = 1, stages = m) of a 2D radius-1 FIXED plan
 // runs in the warp-tile temporal-blocking kernel (tb2d.cuh).
 static TbLaunchFn pick_tb(const Plan* p, int q, int s, int rank, bool wrap) {
@@ -27,6 +21,12 @@ static TbLaunchFn pick_tb(const Plan* p, int q, int s, int rank, bool wrap) {
 }
 
 bool tb_supported(const Plan* p, int q, int s) { return pick_tb(p, q, s, 0, p->boundary == STENCIL_BC_PERIODIC) != nullptr; }
+
+bool sweep_supported(const Plan* p, int q, int s, int rank) {
+    if (rank == 0 && pick_tb(p, q, s, 0, p->boundary == STENCIL_BC_PERIODIC)) return true;
+    if (rank > 0) return s == 1 && p->ndim == 2 && p->r == 1 && pick_cp(p->dtype, q, rank) != nullptr;
+    return pick(p->dtype, p->ndim, p->shape, p->r, q, s) != nullptr;
+}
 
 int launch_sweep(Plan* p, const SweepCall& c) {
     if (TbLaunchFn tb = pick_tb(p, c.q, c.stages, c.rank, c.L->wrap)) {

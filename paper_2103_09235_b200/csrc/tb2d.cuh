@@ -57,11 +57,13 @@ struct TbParams {
     int phys_lo, phys_hi;       // axis-0 faces are physical: frozen ring rows -1 / ny
     int y_lo, y_hi;             // output rows of this launch
     int nstrips, seglen, units;
+    int units_int, seglen_e;    // interior units (strips 1..nstrips-2), edge segment length
+    int x0_right;               // window start of the last strip
     // fused halo exchange (NEXT-2), as SweepParams: outputs of rows j < peer_h
     // (j >= ny - peer_h) are stored again at the same address + peer_dlo (+ peer_dhi) bytes
     long long peer_dlo, peer_dhi;
     int peer_h, peer_lo_on, peer_hi_on;
-    T w[9];                     // taps in canonical order (R4)
+    T w[9];                     // lambda^(1) as the dense 3x3 table, index (dy+1)*3 + (dx+1)
 };
 
 constexpr int TB_D = 16;   // shared row slots per warp (power of two)
@@ -69,12 +71,15 @@ constexpr int TB_D = 16;   // shared row slots per warp (power of two)
 template <typename T, int SHAPE, int K, int VX, int NW>
 struct TbCfg {
     static constexpr int W = 32 * VX;                 // loaded columns per strip
-    static constexpr int WO = W - 2 * K;              // valid output columns per strip
+    static constexpr int EV = 16 / (int)sizeof(T);    // elements per 16-byte vector
+    static constexpr int KA = (K + EV - 1) / EV * EV; // left/right halo, rounded up so every
+                                                      // strip starts 16-byte aligned (vector stores)
+    static constexpr int WO = W - 2 * KA;             // output columns per strip
     static constexpr int D = TB_D;
     static constexpr int PF = (D - K - 1) < 8 ? (D - K - 1) : 8;   // rows in flight ahead
     static constexpr int ROW_BYTES = W * (int)sizeof(T);
-    static constexpr int SMEM = NW * D * ROW_BYTES + NW * D * 8;
-    static constexpr int NTAP = SHAPE == STENCIL_STAR ? 5 : 9;
+    static constexpr int SMEM = D * ROW_BYTES + D * 8;   // one warp per CTA
+    static constexpr int NTAP = 9;   // dense 3x3 (a star uses 5 entries)
     static_assert(K >= 1 && PF >= 2, "temporal block too deep for the slot ring");
     static_assert(W <= 256, "TMA box dimension");
     static_assert((VX * sizeof(T)) % 16 == 0, "16-byte lane vectors");
@@ -133,7 +138,7 @@ struct TbWarp {
     // ring row or a row outside the segment; EDGE: this lane may own a ring column).
     template <bool CHK, bool EDGE>
     __device__ __forceinline__ void row(const T (&w)[C::NTAP], T (&a)[K][VX], T (&b)[K][VX], T (&v)[VX], int i,
-                                        int slot, int eL, int eR) const {
+                                        int slot, unsigned rmask) const {
 #pragma unroll
         for (int s = 0; s < K; ++s) {
             const T vl = __shfl_up_sync(0xffffffffu, v[VX - 1], 1);
@@ -144,10 +149,10 @@ struct TbWarp {
                 const T L = e == 0 ? vl : v[e - 1];
                 const T R = e == VX - 1 ? vr : v[e + 1];
                 if constexpr (SHAPE == STENCIL_STAR) {
-                    // taps: 0 (-1,0)  1 (0,-1)  2 (0,0)  3 (0,1)  4 (1,0)
-                    o[e] = fma(w[4], v[e], a[s][e]);
-                    a[s][e] = fma(w[3], R, fma(w[2], v[e], fma(w[1], L, b[s][e])));
-                    b[s][e] = w[0] * v[e];
+                    // lambda^(1) dense 3x3, index (dy+1)*3 + (dx+1): N 1, W 3, C 4, E 5, S 7
+                    o[e] = fma(w[7], v[e], a[s][e]);
+                    a[s][e] = fma(w[5], R, fma(w[4], v[e], fma(w[3], L, b[s][e])));
+                    b[s][e] = w[1] * v[e];
                 } else {
                     // taps: (dy+1)*3 + (dx+1)
                     o[e] = fma(w[8], R, fma(w[7], v[e], fma(w[6], L, a[s][e])));
@@ -162,12 +167,11 @@ struct TbWarp {
                 const int j = i - (s + 1);
                 if ((p->phys_lo && j == -1) || (p->phys_hi && j == p->ny)) tb_lds<T, VX>(o, srow);
             }
-            if constexpr (EDGE) {
-                if (eL >= 0 || eR >= 0) {
+            if constexpr (EDGE) {   // branch-free: no divergence between the shuffles
+                T r[VX];
+                tb_lds<T, VX>(r, srow);
 #pragma unroll
-                    for (int e = 0; e < VX; ++e)
-                        if (e == eL || e == eR) o[e] = srow[e];
-                }
+                for (int e = 0; e < VX; ++e) o[e] = ((rmask >> e) & 1u) ? r[e] : o[e];
             }
 #pragma unroll
             for (int e = 0; e < VX; ++e) v[e] = o[e];
@@ -181,15 +185,16 @@ struct TbWarp {
         const int i_end = y1 - 1 + K;
         const int nrows = i_end - i_lo + 1;
         const int xl = x0 + lane * VX;
+        // stores: every valid output of the window (overlapping strips write identical values)
         const int vlo = max(x0 + K, 0), vhi = min(x0 + C::W - K, P.nx);
         unsigned smask = 0;
 #pragma unroll
         for (int e = 0; e < VX; ++e)
             if (xl + e >= vlo && xl + e < vhi) smask |= 1u << e;
-        int eL = -1, eR = -1;
+        unsigned rmask = 0;   // elements of this lane that are ring columns (-1 or nx)
         if (EDGE) {
-            if (xl <= -1 && -1 < xl + VX) eL = -1 - xl;
-            if (xl <= P.nx && P.nx < xl + VX) eR = P.nx - xl;
+            if (xl <= -1 && -1 < xl + VX) rmask |= 1u << (-1 - xl);
+            if (xl <= P.nx && P.nx < xl + VX) rmask |= 1u << (P.nx - xl);
         }
         const uint32_t f0 = fill;
         const int ymax = P.ext_y - 1 - (int)P.org_y;   // last allocated row (interior coords)
@@ -220,16 +225,16 @@ struct TbWarp {
             }
             const uint32_t f = f0 + (uint32_t)t;
             const int slot = (int)(f & (C::D - 1));
-            ptx::mbar_wait(&bar[slot], (f / C::D) & 1u);
+            ptx::mbar_wait_spin(&bar[slot], (f / C::D) & 1u);
             T v[VX];
             tb_lds<T, VX>(v, ring + slot * C::W + lane * VX);
             const bool chk = i < y0 + K || (P.phys_hi && i > P.ny);
             bool st = true;
             if (chk) {
-                row<true, EDGE>(w, a, b, v, i, slot, eL, eR);
+                row<true, EDGE>(w, a, b, v, i, slot, rmask);
                 st = i - K >= y0 && i - K < y1;
             } else {
-                row<false, EDGE>(w, a, b, v, i, slot, eL, eR);
+                row<false, EDGE>(w, a, b, v, i, slot, rmask);
             }
             if (st) {
                 const int j = i - K;
@@ -245,17 +250,30 @@ struct TbWarp {
     }
 };
 
+#ifdef TB_PROBE
+// (tuning builds: per-warp smid / start / end / rows, read by stencil_debug_tb_probe)
+static __device__ unsigned long long tb_probe_buf[4 * 8192];   // one per translation unit (fp64: tb2d_f64.cu)
+__device__ __forceinline__ unsigned long long tb_gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#endif
+
+// One warp per CTA (NW = resident CTAs per SM): every warp-level quantity
+// (unit, rows, flags) derives from blockIdx, so the compiler knows it is
+// warp-uniform and emits plain SHFLs without divergence checks.
 template <typename T, int SHAPE, int K, int VX, int NW>
-__global__ void __launch_bounds__(NW * 32, 1)
+__global__ void __launch_bounds__(32, NW)
     tb2d_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TbParams<T> p) {
     using C = TbCfg<T, SHAPE, K, VX, NW>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int lane = threadIdx.x;
     TbWarp<T, SHAPE, K, VX, NW> tw;
     tw.tmap = &tmap;
     tw.p = &p;
-    tw.ring = reinterpret_cast<T*>(smem_raw) + (size_t)warp * C::D * C::W;
-    tw.bar = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NW * C::D * C::ROW_BYTES) + warp * C::D;
+    tw.ring = reinterpret_cast<T*>(smem_raw);
+    tw.bar = reinterpret_cast<uint64_t*>(smem_raw + (size_t)C::D * C::ROW_BYTES);
     tw.lane = lane;
     tw.fill = 0;
     if (lane == 0) {
@@ -268,16 +286,42 @@ __global__ void __launch_bounds__(NW * 32, 1)
     T w[C::NTAP];
 #pragma unroll
     for (int k = 0; k < C::NTAP; ++k) w[k] = p.w[k];
-    const int nwt = gridDim.x * NW;
-    for (int u = blockIdx.x * NW + warp; u < p.units; u += nwt) {
-        const int strip = u % p.nstrips, seg = u / p.nstrips;
-        const int y0 = p.y_lo + seg * p.seglen;
-        const int y1 = min(y0 + p.seglen, p.y_hi);
-        const int x0 = strip * C::WO - K;
+#ifdef TB_PROBE
+    const unsigned long long t_start = tb_gtime();
+#endif
+    for (int u = blockIdx.x; u < p.units; u += gridDim.x) {
+        // interior strips first (segments of seglen rows), then the two edge
+        // strips in segments of seglen_e rows (their ring-column handling
+        // costs more per row, so they get shorter segments: no tail)
+        int strip, y0, y1;
+        if (u < p.units_int) {
+            strip = p.nstrips > 2 ? 1 + u % (p.nstrips - 2) : 0;
+            y0 = p.y_lo + (u / (p.nstrips - 2)) * p.seglen;
+            y1 = min(y0 + p.seglen, p.y_hi);
+        } else {
+            const int e = u - p.units_int;
+            strip = p.nstrips == 1 ? 0 : (e % 2) * (p.nstrips - 1);
+            y0 = p.y_lo + (p.nstrips == 1 ? e : e / 2) * p.seglen_e;
+            y1 = min(y0 + p.seglen_e, p.y_hi);
+        }
+        // strips 0 .. nstrips-2 advance by WO from x = -KA; the last one is placed
+        // (host) so that its window holds column nx and overlaps its neighbour
+        const int x0 = (strip == p.nstrips - 1 && p.nstrips > 1) ? p.x0_right : strip * C::WO - C::KA;
         const bool edge = x0 <= -1 || x0 + C::W > p.nx;   // the window holds a ring column
         if (edge) tw.template unit<true>(w, x0, y0, y1);
         else tw.template unit<false>(w, x0, y0, y1);
     }
+#ifdef TB_PROBE
+    const int gw = blockIdx.x;
+    if (lane == 0 && gw < 8192) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+        tb_probe_buf[4 * gw + 0] = smid;
+        tb_probe_buf[4 * gw + 1] = t_start;
+        tb_probe_buf[4 * gw + 2] = tb_gtime();
+        tb_probe_buf[4 * gw + 3] = tw.fill;
+    }
+#endif
 }
 
 // ------------------------------------------------------------------ host
@@ -307,7 +351,7 @@ int tb2d_launch(Plan* p, const SweepCall& c) {
     prm.y_hi = (int)bx.hi[0];
     if (!L.phys_lo[0] && L.lo_valid[0] < K) return set_error(STENCIL_EUNSUPPORTED, "tb2d: ghost rows < fold_m");
     if (!L.phys_hi[0] && L.hi_valid[0] < K) return set_error(STENCIL_EUNSUPPORTED, "tb2d: ghost rows < fold_m");
-    if ((int)c.coef->size() != C::NTAP) return set_error(STENCIL_EUNSUPPORTED, "tb2d: tap count");
+    if ((int)c.coef->size() != C::NTAP) return set_error(STENCIL_EUNSUPPORTED, "tb2d: expected the dense 3x3 lambda^(1)");
     for (int k = 0; k < C::NTAP; ++k) prm.w[k] = static_cast<T>((*c.coef)[k]);
     if (c.peer_h > 0) {
         const long long plane = (long long)L.n[0] * L.stride[0] * (long long)sizeof(T);
@@ -320,18 +364,37 @@ int tb2d_launch(Plan* p, const SweepCall& c) {
             prm.peer_dhi = (long long)(reinterpret_cast<intptr_t>(c.peer_hi) - reinterpret_cast<intptr_t>(c.dst)) - plane;
     }
     const int rows = prm.y_hi - prm.y_lo;
-    const int nstrips = (prm.nx + C::WO - 1) / C::WO;
+    // strips: x0 = s WO - KA while the window stays left of the ring column nx;
+    // then one last strip whose window holds nx, starting no later than the
+    // next regular one (so the valid outputs cover [0, nx) without a gap)
+    int nstrips = 1, xlast = -C::KA;
+    if (xlast + C::W <= prm.nx) {
+        while (xlast + C::WO + C::W <= prm.nx) {
+            xlast += C::WO;
+            ++nstrips;
+        }
+        int xr = prm.nx + C::KA + 1 - C::W;
+        xr = (xr >= 0 ? xr / C::EV : -((-xr + C::EV - 1) / C::EV)) * C::EV;   // align down
+        prm.x0_right = std::min(xr, xlast + C::WO);
+        ++nstrips;
+    }
     const int warps = std::max(1, p->sm_count) * NW;
     // segments: about one unit per resident warp, but at least 4K rows each
-    // (a segment re-loads and re-computes 2K rows of pipeline fill)
-    int nseg = std::max(1, warps / nstrips);
+    // (a segment re-loads and re-computes 2K rows of pipeline fill); the two
+    // edge strips get segments of half the length (2 nseg units each)
+    const int nint = nstrips > 2 ? nstrips - 2 : 0, nedge = nstrips > 2 ? 2 : nstrips;
+    int nseg = std::max(1, warps / (nint + 2 * nedge));
     nseg = std::min(nseg, std::max(1, rows / (4 * K)));
     const int seglen = (rows + nseg - 1) / nseg;
     nseg = (rows + seglen - 1) / seglen;
+    const int seglen_e = std::max(1, (seglen + 1) / 2);
+    const int nseg_e = (rows + seglen_e - 1) / seglen_e;
     prm.nstrips = nstrips;
     prm.seglen = seglen;
-    prm.units = nstrips * nseg;
-    const int grid = std::max(1, std::min(std::max(1, p->sm_count), (prm.units + NW - 1) / NW));
+    prm.seglen_e = seglen_e;
+    prm.units_int = nint * nseg;
+    prm.units = nint * nseg + nedge * nseg_e;
+    const int grid = std::max(1, std::min(warps, prm.units));   // one warp per CTA, NW CTAs per SM
 
     auto enc = tb_encode_fn();
     if (!enc) return set_error(STENCIL_ECUDA, "cuTensorMapEncodeTiled not available from the driver");
@@ -357,7 +420,7 @@ int tb2d_launch(Plan* p, const SweepCall& c) {
             done[dev] = true;
         }
     }
-    tb2d_kernel<T, SHAPE, K, VX, NW><<<grid, NW * 32, C::SMEM, (cudaStream_t)c.stream>>>(map, prm);
+    tb2d_kernel<T, SHAPE, K, VX, NW><<<grid, 32, C::SMEM, (cudaStream_t)c.stream>>>(map, prm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "tb2d_kernel launch");
     return 1;

@@ -17,6 +17,20 @@ PFN_cuTensorMapEncodeTiled_v12000 tb_encode_fn() {
     return fn;
 }
 
+#ifdef TB_PROBE
+}  // namespace sb
+extern "C" int stencil_debug_tb_probe(unsigned long long* host, int n, int reset) {
+    cudaDeviceSynchronize();
+    cudaError_t e = cudaMemcpyFromSymbol(host, sb::tb_probe_buf, sizeof(unsigned long long) * 4 * (size_t)n);
+    if (reset) {
+        static unsigned long long zero[4 * 8192] = {};
+        cudaMemcpyToSymbol(sb::tb_probe_buf, zero, sizeof(zero));
+    }
+    return e == cudaSuccess ? 0 : -3;
+}
+namespace sb {
+#endif
+
 #ifndef TB_F64_VX
 #define TB_F64_VX 4
 #endif
