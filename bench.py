@@ -41,15 +41,14 @@ CONFIGS = {
     # best_m: the fold_m measured fastest on B200 (bench.py --fold-m 0 re-measures all of `ms`)
     "c1": dict(name="1D3P heat fp64 N=100000 T=100", dims=(100000,), shape="star", dtype="f64", T=100, ms=(1, 2),
                best_m=2),
-    # fold_m = 3 is not in BASELINE's list {1, 2, 4} for this config; the folding works for
-    # any m (T = 200 = 66 sweeps of lambda^(3) + one of lambda^(2), R10) and m = 3 balances the
-    # 25-tap fold against HBM: 0.77-0.83 of the HBM roofline (m = 4: 0.58) at the same
-    # throughput within 2% (983 vs 953 in short runs; 918 vs 938 in 20-step runs, where
-    # m = 3's higher HBM power pulls the SM clock to ~1.7 GHz under sw_power_cap)
+    # fold_m = 8 (C2, C3): the on-chip temporal block (stages = m; NEXT-1 / a6)
+    # applies 8 single steps per HBM round trip: T = 200 = 25 sweeps.  BASELINE lists fold_m
+    # in {1, 2, 4}; every fold gives the same result (R10), and --fold-m 0 measures m = 1, 2,
+    # 3, 4 (the folded passes) beside it.  Round 1's best was the folded m = 3 (1006).
     "c2": dict(name="2D5P star fp64 8192x8192 T=200", dims=(8192, 8192), shape="star", dtype="f64", T=200,
-               ms=(1, 2, 3, 4), best_m=3),
+               ms=(1, 2, 3, 4, 8), best_m=8),
     "c3": dict(name="2D9P box fp32 16384x16384 T=200", dims=(16384, 16384), shape="box", dtype="f32", T=200,
-               ms=(1, 2, 4), best_m=2),
+               ms=(1, 2, 4, 8), best_m=8),
     "c4": dict(name="3D7P star fp64 512^3 T=100", dims=(512, 512, 512), shape="star", dtype="f64", T=100,
                ms=(1, 2), best_m=2),
     "c5": dict(name="3D27P box fp64 768x768x384 T=100", dims=(384, 768, 768), shape="box", dtype="f64", T=100,
@@ -574,12 +573,16 @@ def run_ours(args):
     frac_f = fma_ach / fma_peak if fma_ach else None
     alu_bound = frac_f is not None and frac_h is not None and frac_f > frac_h
     key = "%s/m%d/s%d" % (args.config, m, args.stages)
+    var = plan.variant(m) if nd >= 2 and args.stages == 0 else None
+    tb = nd == 2 and m > 1 and ((var is not None and var[0] == 1 and var[1] == m) or args.stages == m)
+    kernel_name = ("tb2d_kernel (on-chip temporal block, %d steps per HBM round trip)" % m if tb else
+                   "onchip1d_kernel (fold_m=%d)" % m if nd == 1 else "sweep_kernel (main region, fold_m=%d)" % m)
     roof = {"bound": "alu" if alu_bound else "hbm",
             "achieved": (fma_ach if alu_bound else ach), "peak": (fma_peak if alu_bound else hbm_peak),
             "unit": "TFMA/s" if alu_bound else "GB/s",
             "frac": (frac_f if alu_bound else frac_h),
             "traffic": traffic_lookup(key),
-            "kernel": "sweep_kernel (main region, fold_m=%d)" % m,
+            "kernel": kernel_name,
             "peak_kind": peak_kind if not alu_bound else "derived: 148 SM x %d FMA/clk x %.0f MHz" % (fma_per_clk, sm_max),
             "hbm": {"achieved_gbs": ach, "peak_gbs": hbm_peak, "frac": frac_h},
             "fma": {"achieved_tfma_s": fma_ach, "peak_tfma_s": fma_peak, "frac": frac_f},

@@ -88,6 +88,7 @@ void to_public(const Layout3& L, stencil_layout* out);
 // then the vertical fold of the counterparts into the window (2D only).
 struct Variant { int q; int stages; int rank = 0; };
 Variant choose_variant(Plan* p, int m);
+bool tb_supported(const Plan* p, int q, int s);   // 2D temporal block compiled for (q = 1, s steps)
 int auto_fold(Plan* p);   // fold_m = 0 in a run: the measured-best fold for the family
 
 // Counterpart decomposition of the 2D folded matrix Lambda = lambda^(q)

@@ -175,6 +175,13 @@ Variant choose_variant(Plan* p, int m) {
         if (lr.rank >= 1 && lr.rank <= STENCIL_MAX_COUNTERPARTS && 2 * W * lr.rank < full)
             return Variant{m, 1, lr.rank};
     }
+    // 2D radius-1 FIXED plans: the warp-tile temporal block (tb2d.cuh, m single
+    // steps per HBM round trip, stages = m) beats one folded pass from m = 4
+    // (stars) / m = 3 (boxes) on -- measured on B200 (C2 m=4
+    // 1140 vs 983, m=3 822 vs 1016; C3 m=3 1306 vs 983, m=2 963 vs 1428).
+    if (p->ndim == 2 && p->r == 1 && p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, m) &&
+        (m >= 4 || (m == 3 && p->shape == STENCIL_BOX)))
+        return {1, m};
     if (full <= 64) return {m, 1};
     Variant best = {m, 1};
     double best_cost = 1e30;
@@ -287,6 +294,7 @@ int auto_fold(Plan* p) {
         if (p->counterparts && lowrank(p, 4).rank >= 1 && lowrank(p, 4).rank <= STENCIL_MAX_COUNTERPARTS &&
             2 * 9 * lowrank(p, 4).rank < support_size(2, p->shape, 1, 4))
             return 4;                                    // counterparts: 18 FMAs per point for 4 steps
+        if (p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 8)) return 8;   // temporal block, 8 steps
         if (p->shape == STENCIL_STAR) return 3;
         return 2;
     }

@@ -76,7 +76,12 @@ struct TbCfg {
                                                       // strip starts 16-byte aligned (vector stores)
     static constexpr int WO = W - 2 * KA;             // output columns per strip
     static constexpr int D = TB_D;
-    static constexpr int PF = (D - K - 1) < 8 ? (D - K - 1) : 8;   // rows in flight ahead
+#ifndef TB_G
+#define TB_G 2
+#endif
+    static constexpr int G = (K % TB_G == 0 && K >= TB_G) ? TB_G : 1;   // stage groups (skew)
+    static constexpr int LAG = K + G - 1;                      // rows between load and final output
+    static constexpr int PF = (D - LAG - 1) < 8 ? (D - LAG - 1) : 8;   // rows in flight ahead
     static constexpr int ROW_BYTES = W * (int)sizeof(T);
     static constexpr int SMEM = D * ROW_BYTES + D * 8;   // one warp per CTA
     static constexpr int NTAP = 9;   // dense 3x3 (a star uses 5 entries)
@@ -134,47 +139,74 @@ struct TbWarp {
     int lane;
     uint32_t fill;    // rows issued so far (slot = fill % D, parity = fill / D % 2)
 
-    // One row of level 0 through the K stages (CHK: the iteration may output a
-    // ring row or a row outside the segment; EDGE: this lane may own a ring column).
+    // One stage: input row v (level s), state (a, b), output o = level s+1 of
+    // row j (frozen ring cells keep u0, re-read from the row's shared slot).
     template <bool CHK, bool EDGE>
-    __device__ __forceinline__ void row(const T (&w)[C::NTAP], T (&a)[K][VX], T (&b)[K][VX], T (&v)[VX], int i,
-                                        int slot, unsigned rmask) const {
+    __device__ __forceinline__ void stage(const T (&w)[C::NTAP], T (&a)[VX], T (&b)[VX], const T (&v)[VX], T (&o)[VX],
+                                          int j, int sl, unsigned rmask) const {
+        const T vl = __shfl_up_sync(0xffffffffu, v[VX - 1], 1);
+        const T vr = __shfl_down_sync(0xffffffffu, v[0], 1);
 #pragma unroll
-        for (int s = 0; s < K; ++s) {
-            const T vl = __shfl_up_sync(0xffffffffu, v[VX - 1], 1);
-            const T vr = __shfl_down_sync(0xffffffffu, v[0], 1);
-            T o[VX];
+        for (int e = 0; e < VX; ++e) {
+            const T L = e == 0 ? vl : v[e - 1];
+            const T R = e == VX - 1 ? vr : v[e + 1];
+            // (terms in v first, the shuffled neighbours L, R last: the
+            // shuffle latency overlaps the first multiply-add)
+            if constexpr (SHAPE == STENCIL_STAR) {
+                // lambda^(1) dense 3x3, index (dy+1)*3 + (dx+1): N 1, W 3, C 4, E 5, S 7
+                o[e] = fma(w[7], v[e], a[e]);
+                a[e] = fma(w[5], R, fma(w[3], L, fma(w[4], v[e], b[e])));
+                b[e] = w[1] * v[e];
+            } else {
+                // taps: (dy+1)*3 + (dx+1)
+                o[e] = fma(w[8], R, fma(w[6], L, fma(w[7], v[e], a[e])));
+                a[e] = fma(w[5], R, fma(w[3], L, fma(w[4], v[e], b[e])));
+                b[e] = fma(w[2], R, fma(w[0], L, w[1] * v[e]));
+            }
+        }
+        const T* srow = ring + sl * C::W + lane * VX;
+        if constexpr (CHK) {
+            if ((p->phys_lo && j == -1) || (p->phys_hi && j == p->ny)) tb_lds<T, VX>(o, srow);
+        }
+        if constexpr (EDGE) {   // branch-free: no divergence between the shuffles
+            T r[VX];
+            tb_lds<T, VX>(r, srow);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) o[e] = ((rmask >> e) & 1u) ? r[e] : o[e];
+        }
+    }
+
+    // One iteration: the K stages in G groups of K/G.  Group g works one row
+    // behind group g-1 (its input is pend[g-1], group g-1's output of the
+    // previous iteration), so the groups are independent within the
+    // iteration and their dependent chains interleave (ILP).  Stage s (group
+    // g) outputs row j = i - g - s - 1.  On return v holds the level-K row
+    // i - K - (G-1).
+    template <bool CHK, bool EDGE>
+    __device__ __forceinline__ void row(const T (&w)[C::NTAP], T (&a)[K][VX], T (&b)[K][VX], T (&pend)[C::G][VX],
+                                        T (&v)[VX], int i, int slot, unsigned rmask) const {
+        T v0[VX];   // the loaded row (v is overwritten by the last group, which runs first)
+#pragma unroll
+        for (int e = 0; e < VX; ++e) v0[e] = v[e];
+        constexpr int KG = K / C::G;
+#pragma unroll
+        for (int g = C::G - 1; g >= 0; --g) {
+            T x[VX];
+#pragma unroll
+            for (int e = 0; e < VX; ++e) x[e] = g == 0 ? v0[e] : pend[g - 1][e];
+#pragma unroll
+            for (int q = 0; q < KG; ++q) {
+                const int s = g * KG + q;
+                T o[VX];
+                stage<CHK, EDGE>(w, a[s], b[s], x, o, i - g - s - 1, (slot - g - s - 1) & (C::D - 1), rmask);
+#pragma unroll
+                for (int e = 0; e < VX; ++e) x[e] = o[e];
+            }
 #pragma unroll
             for (int e = 0; e < VX; ++e) {
-                const T L = e == 0 ? vl : v[e - 1];
-                const T R = e == VX - 1 ? vr : v[e + 1];
-                if constexpr (SHAPE == STENCIL_STAR) {
-                    // lambda^(1) dense 3x3, index (dy+1)*3 + (dx+1): N 1, W 3, C 4, E 5, S 7
-                    o[e] = fma(w[7], v[e], a[s][e]);
-                    a[s][e] = fma(w[5], R, fma(w[4], v[e], fma(w[3], L, b[s][e])));
-                    b[s][e] = w[1] * v[e];
-                } else {
-                    // taps: (dy+1)*3 + (dx+1)
-                    o[e] = fma(w[8], R, fma(w[7], v[e], fma(w[6], L, a[s][e])));
-                    a[s][e] = fma(w[5], R, fma(w[4], v[e], fma(w[3], L, b[s][e])));
-                    b[s][e] = fma(w[2], R, fma(w[1], v[e], w[0] * L));
-                }
+                if (g == C::G - 1) v[e] = x[e];
+                else pend[g][e] = x[e];
             }
-            // o = level s+1, row i-(s+1): frozen ring cells keep u0 (re-read from the slot)
-            const int sl = (slot - (s + 1)) & (C::D - 1);
-            const T* srow = ring + sl * C::W + lane * VX;
-            if constexpr (CHK) {
-                const int j = i - (s + 1);
-                if ((p->phys_lo && j == -1) || (p->phys_hi && j == p->ny)) tb_lds<T, VX>(o, srow);
-            }
-            if constexpr (EDGE) {   // branch-free: no divergence between the shuffles
-                T r[VX];
-                tb_lds<T, VX>(r, srow);
-#pragma unroll
-                for (int e = 0; e < VX; ++e) o[e] = ((rmask >> e) & 1u) ? r[e] : o[e];
-            }
-#pragma unroll
-            for (int e = 0; e < VX; ++e) v[e] = o[e];
         }
     }
 
@@ -182,7 +214,7 @@ struct TbWarp {
     __device__ __forceinline__ void unit(const T (&w)[C::NTAP], int x0, int y0, int y1) {
         const TbParams<T>& P = *p;
         const int i_lo = (P.phys_lo && y0 - K < -1) ? -1 : y0 - K;
-        const int i_end = y1 - 1 + K;
+        const int i_end = y1 - 1 + C::LAG;
         const int nrows = i_end - i_lo + 1;
         const int xl = x0 + lane * VX;
         // stores: every valid output of the window (overlapping strips write identical values)
@@ -210,12 +242,19 @@ struct TbWarp {
             ptx::fence_proxy_async();
             for (int t = 0; t < min(C::PF, nrows); ++t) issue(t);
         }
-        T a[K][VX], b[K][VX];
+        T a[K][VX], b[K][VX], pend[C::G][VX];
 #pragma unroll
         for (int s = 0; s < K; ++s)
 #pragma unroll
             for (int e = 0; e < VX; ++e) a[s][e] = b[s][e] = T(0);
-        T* g = P.dst + (P.org_y + (long long)(i_lo - K)) * P.pitch + P.org_x + xl;   // row i - K
+#pragma unroll
+        for (int q = 0; q < C::G; ++q)
+#pragma unroll
+            for (int e = 0; e < VX; ++e) pend[q][e] = T(0);
+        T* g = P.dst + (P.org_y + (long long)(i_lo - C::LAG)) * P.pitch + P.org_x + xl;   // row i - LAG
+#if defined(TB_UNROLL) && TB_UNROLL == 2
+#pragma unroll 2
+#endif
         for (int t = 0; t < nrows; ++t) {
             const int i = i_lo + t;
             __syncwarp();
@@ -228,16 +267,16 @@ struct TbWarp {
             ptx::mbar_wait_spin(&bar[slot], (f / C::D) & 1u);
             T v[VX];
             tb_lds<T, VX>(v, ring + slot * C::W + lane * VX);
-            const bool chk = i < y0 + K || (P.phys_hi && i > P.ny);
+            const bool chk = i < y0 + C::LAG || (P.phys_hi && i > P.ny);
             bool st = true;
             if (chk) {
-                row<true, EDGE>(w, a, b, v, i, slot, rmask);
-                st = i - K >= y0 && i - K < y1;
+                row<true, EDGE>(w, a, b, pend, v, i, slot, rmask);
+                st = i - C::LAG >= y0 && i - C::LAG < y1;
             } else {
-                row<false, EDGE>(w, a, b, v, i, slot, rmask);
+                row<false, EDGE>(w, a, b, pend, v, i, slot, rmask);
             }
             if (st) {
-                const int j = i - K;
+                const int j = i - C::LAG;
                 tb_stg<T, VX>(g, v, smask);
                 if (P.peer_lo_on && j < P.peer_h)
                     tb_stg<T, VX>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dlo), v, smask);

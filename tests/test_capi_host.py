@@ -211,9 +211,16 @@ def test_new_entry_points_validate_arguments():
 def test_auto_fold_table():
     """fold_m = 0 (auto): the measured-best fold per family."""
     assert Plan((100,), 1, "star", synth.weights(3, 1)).auto_fold() == 2
-    assert Plan((64, 64), 1, "star", synth.weights(5, 1)).auto_fold() == 3
-    assert Plan((64, 64), 1, "star", synth.weights(5, 1), dtype="f32").auto_fold() == 3
-    assert Plan((64, 64), 1, "box", synth.weights(9, 1), dtype="f32").auto_fold() == 2
+    assert Plan((64, 64), 1, "star", synth.weights(5, 1)).auto_fold() == 8             # temporal block
+    assert Plan((64, 64), 1, "star", synth.weights(5, 1), dtype="f32").auto_fold() == 8
+    assert Plan((64, 64), 1, "box", synth.weights(9, 1), dtype="f32").auto_fold() == 8
     assert Plan((64, 64), 1, "box", [1.0 / 9] * 9, dtype="f32").auto_fold() == 4      # counterparts
+    assert Plan((64, 64), 1, "star", synth.weights(5, 1), boundary="periodic").auto_fold() == 3
+    assert Plan((64, 64), 1, "box", synth.weights(9, 1), boundary="periodic").auto_fold() == 2
+    # variant policy: temporal block (q = 1, stages = m) for m >= 4 (stars) / m >= 3 (boxes)
+    st = Plan((64, 64), 1, "star", synth.weights(5, 1))
+    bx = Plan((64, 64), 1, "box", synth.weights(9, 1), dtype="f32")
+    assert st.variant(3) == (3, 1, 0) and st.variant(4) == (1, 4, 0) and st.variant(8) == (1, 8, 0)
+    assert bx.variant(2) == (2, 1, 0) and bx.variant(3) == (1, 3, 0)
     assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1)).auto_fold() == 2
     assert Plan((16, 16, 16), 1, "box", synth.weights(27, 1)).auto_fold() == 1

@@ -1,0 +1,16 @@
+# usage: bash tools/tbtune.sh lib1 lib2 ...   (tunelibs/lib_<name>.so; "main" = in-tree library)
+for name in "$@"; do
+  if [ "$name" = main ]; then unset STENCIL_B200_LIB; else export STENCIL_B200_LIB=tunelibs/lib_$name.so; fi
+  for cfg in "c2 8" "c3 8" "c2 6"; do set -- $cfg
+    timeout 120 python bench.py --config $1 --fold-m $2 --stages $2 --steps 5 --headline-only --no-cpu-baseline > gpurun_out/tt_${name}_$1_k$2.json 2>gpurun_out/tt_${name}_$1_k$2.err
+  done
+done
+python - <<'PY'
+import glob, json
+for f in sorted(glob.glob("gpurun_out/tt_*.json")):
+    try:
+        d = json.loads(open(f).read().strip().splitlines()[-1]); r = d["roofline"]
+        print(f.split("/")[-1], round(d["value"], 1), "hbm", round(r["hbm"]["frac"], 3), "fma", round(r["fma"]["frac"], 3), d["clocks"].get("sm_mhz"))
+    except Exception as e:
+        print(f, "ERR", open(f.replace(".json", ".err")).read()[-200:])
+PY
