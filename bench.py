@@ -60,7 +60,7 @@ CONFIGS = {
                 shape="box", dtype="f32", T=200, ms=(1, 2, 4), best_m=4, weights="uniform"),
 }
 SAMPLE = {  # oracle sub-window of each workload for the CPU baseline / reference arm
-    "c1": (100000,), "c2": (1024, 1024), "c3": (1024, 1024), "c4": (96, 96, 96), "c5": (64, 64, 64),
+    "c1": (100000,), "c2": (4096, 4096), "c3": (4096, 4096), "c4": (192, 192, 192), "c5": (128, 128, 128),
     "c3u": (1024, 1024),
 }
 

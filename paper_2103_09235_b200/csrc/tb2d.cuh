@@ -302,8 +302,13 @@ __device__ __forceinline__ unsigned long long tb_gtime() {
 // One warp per CTA (NW = resident CTAs per SM): every warp-level quantity
 // (unit, rows, flags) derives from blockIdx, so the compiler knows it is
 // warp-uniform and emits plain SHFLs without divergence checks.
+#ifdef TB_MAXNREG
+#define TB_REGS __maxnreg__(TB_MAXNREG)
+#else
+#define TB_REGS __launch_bounds__(32, NW)
+#endif
 template <typename T, int SHAPE, int K, int VX, int NW>
-__global__ void __launch_bounds__(32, NW)
+__global__ void TB_REGS
     tb2d_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ TbParams<T> p) {
     using C = TbCfg<T, SHAPE, K, VX, NW>;
     extern __shared__ __align__(128) unsigned char smem_raw[];

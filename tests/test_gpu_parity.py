@@ -187,7 +187,9 @@ def test_errors_and_launch_count():
     with pytest.raises(StencilError):
         plan.run(a, b, -1, 1, workspace=None)
     with pytest.raises(StencilError):
-        plan.run(a, b, 4, 0, workspace=None)
+        plan.run(a, b, 4, -1, workspace=None)        # fold_m < 0 (0 = auto)
+    with pytest.raises(StencilError):
+        plan.run(a, b, 20, 0, workspace=None)        # auto fold (8): 3 sweeps need a workspace
     with pytest.raises(StencilError):
         plan.run(a, b, 8, 2, workspace=None)         # needs a workspace
     with pytest.raises(StencilError):

@@ -63,7 +63,7 @@ def test_schedule_paths_whole_frame(dims, shape, dtype, T, m, max_ctas):
     plan.run(a, b, 1, 1, workspace=ws)          # allocate the schedule scratch
     torch.cuda.synchronize()
     plan.sched_stats(reset=True)
-    plan.run(a, b, T, m, workspace=ws)
+    plan.run(a, b, T, m, workspace=ws, stages=1)   # the folded pass: the dynamic-schedule kernel
     torch.cuda.synchronize()
     grabs, steals = plan.sched_stats()
     got = plan.frame_view(b).cpu().double().numpy()
