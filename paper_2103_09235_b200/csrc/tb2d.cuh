@@ -40,6 +40,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <type_traits>
 
 #include "internal.hpp"
 #include "ptx.cuh"
@@ -67,6 +68,9 @@ struct TbParams {
 };
 
 constexpr int TB_D = 16;   // shared row slots per warp (power of two)
+#ifndef TB_FFMA2
+#define TB_FFMA2 0         // fp32 element pairs with packed FFMA2: measured slower
+#endif
 
 template <typename T, int SHAPE, int K, int VX, int NW>
 struct TbCfg {
@@ -85,12 +89,16 @@ struct TbCfg {
     static constexpr int ROW_BYTES = W * (int)sizeof(T);
     static constexpr int SMEM = D * ROW_BYTES + D * 8;   // one warp per CTA
     static constexpr int NTAP = 9;   // dense 3x3 (a star uses 5 entries)
+    // register element: fp32 pairs (packed FFMA2 on sm_100) or one scalar
+    static constexpr bool FP2 = sizeof(T) == 4 && TB_FFMA2;
+    using E = std::conditional_t<FP2, float2, T>;
+    static constexpr int NE = FP2 ? VX / 2 : VX;   // elements per lane
     static_assert(K >= 1 && PF >= 2, "temporal block too deep for the slot ring");
     static_assert(W <= 256, "TMA box dimension");
     static_assert((VX * sizeof(T)) % 16 == 0, "16-byte lane vectors");
 };
 
-template <typename T, int VX>
+template <int VX, typename T>
 __device__ __forceinline__ void tb_lds(T (&v)[VX], const T* s) {
     constexpr int NV = VX * (int)sizeof(T) / 16;
 #pragma unroll
@@ -109,7 +117,7 @@ __device__ __forceinline__ void tb_lds(T (&v)[VX], const T* s) {
     }
 }
 
-template <typename T, int VX>
+template <int VX, typename T>
 __device__ __forceinline__ void tb_stg(T* g, const T (&v)[VX], unsigned mask) {
     constexpr int EV = 16 / (int)sizeof(T);   // elements per 16-byte vector
     constexpr unsigned FULL = (1u << EV) - 1u;
@@ -129,6 +137,47 @@ __device__ __forceinline__ void tb_stg(T* g, const T (&v)[VX], unsigned mask) {
     }
 }
 
+// fp32 element pairs: the lane's VX floats (columns c .. c+VX-1) are held as
+// VX/2 float2 pairs P[q] = (column c+q, column c+q+VX/2).  Then the west
+// neighbour pair of P[q] is P[q-1] and the east one P[q+1]: only the two end
+// pairs are assembled from shuffled values, so packed FFMA2 needs almost no
+// register moves.
+template <int NE>
+__device__ __forceinline__ void tb_lds(float2 (&v)[NE], const float* s) {
+    static_assert(NE % 4 == 0, "fp32 pairs: VX multiple of 8");
+#pragma unroll
+    for (int q = 0; q < NE; q += 4) {
+        const float4 lo = reinterpret_cast<const float4*>(s)[q / 4];
+        const float4 hi = reinterpret_cast<const float4*>(s + NE)[q / 4];
+        v[q] = make_float2(lo.x, hi.x);
+        v[q + 1] = make_float2(lo.y, hi.y);
+        v[q + 2] = make_float2(lo.z, hi.z);
+        v[q + 3] = make_float2(lo.w, hi.w);
+    }
+}
+
+template <int NE>
+__device__ __forceinline__ void tb_stg(float* g, const float2 (&v)[NE], unsigned mask) {
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int q = 0; q < NE; q += 4) {
+            const int e0 = h * NE + q;   // first column of this 16-byte vector
+            const unsigned mq = (mask >> e0) & 15u;
+            const float f0 = h ? v[q].y : v[q].x, f1 = h ? v[q + 1].y : v[q + 1].x;
+            const float f2 = h ? v[q + 2].y : v[q + 2].x, f3 = h ? v[q + 3].y : v[q + 3].x;
+            if (mq == 15u) {
+                reinterpret_cast<float4*>(g + e0)[0] = make_float4(f0, f1, f2, f3);
+            } else if (mq) {
+                const float f[4] = {f0, f1, f2, f3};
+#pragma unroll
+                for (int e = 0; e < 4; ++e)
+                    if (mq & (1u << e)) g[e0 + e] = f[e];
+            }
+        }
+    }
+}
+
 template <typename T, int SHAPE, int K, int VX, int NW>
 struct TbWarp {
     using C = TbCfg<T, SHAPE, K, VX, NW>;
@@ -141,38 +190,72 @@ struct TbWarp {
 
     // One stage: input row v (level s), state (a, b), output o = level s+1 of
     // row j (frozen ring cells keep u0, re-read from the row's shared slot).
+    using E = typename C::E;
+    static constexpr int NE = C::NE;
+
     template <bool CHK, bool EDGE>
-    __device__ __forceinline__ void stage(const T (&w)[C::NTAP], T (&a)[VX], T (&b)[VX], const T (&v)[VX], T (&o)[VX],
+    __device__ __forceinline__ void stage(const T (&w)[C::NTAP], E (&a)[NE], E (&b)[NE], const E (&v)[NE], E (&o)[NE],
                                           int j, int sl, unsigned rmask) const {
-        const T vl = __shfl_up_sync(0xffffffffu, v[VX - 1], 1);
-        const T vr = __shfl_down_sync(0xffffffffu, v[0], 1);
+        if constexpr (C::FP2) {
+            // fp32 pairs P[q] = (column q, column q + NE): west neighbour pair P[q-1],
+            // east P[q+1]; the end pairs take the lane neighbours' end columns
+            const float vl = __shfl_up_sync(0xffffffffu, v[NE - 1].y, 1);   // column -1
+            const float vr = __shfl_down_sync(0xffffffffu, v[0].x, 1);      // column VX
+            const float2 Wst = make_float2(vl, v[NE - 1].x);                  // west of P[0]
+            const float2 Est = make_float2(v[0].y, vr);                       // east of P[NE-1]
+            auto W2 = [&](int k) { return make_float2(w[k], w[k]); };
 #pragma unroll
-        for (int e = 0; e < VX; ++e) {
-            const T L = e == 0 ? vl : v[e - 1];
-            const T R = e == VX - 1 ? vr : v[e + 1];
-            // (terms in v first, the shuffled neighbours L, R last: the
-            // shuffle latency overlaps the first multiply-add)
-            if constexpr (SHAPE == STENCIL_STAR) {
-                // lambda^(1) dense 3x3, index (dy+1)*3 + (dx+1): N 1, W 3, C 4, E 5, S 7
-                o[e] = fma(w[7], v[e], a[e]);
-                a[e] = fma(w[5], R, fma(w[3], L, fma(w[4], v[e], b[e])));
-                b[e] = w[1] * v[e];
-            } else {
-                // taps: (dy+1)*3 + (dx+1)
-                o[e] = fma(w[8], R, fma(w[6], L, fma(w[7], v[e], a[e])));
-                a[e] = fma(w[5], R, fma(w[3], L, fma(w[4], v[e], b[e])));
-                b[e] = fma(w[2], R, fma(w[0], L, w[1] * v[e]));
+            for (int q = 0; q < NE; ++q) {
+                const float2 L = q == 0 ? Wst : v[q - 1];
+                const float2 R = q == NE - 1 ? Est : v[q + 1];
+                if constexpr (SHAPE == STENCIL_STAR) {
+                    o[q] = __ffma2_rn(W2(7), v[q], a[q]);
+                    a[q] = __ffma2_rn(W2(5), R, __ffma2_rn(W2(3), L, __ffma2_rn(W2(4), v[q], b[q])));
+                    b[q] = __fmul2_rn(W2(1), v[q]);
+                } else {
+                    o[q] = __ffma2_rn(W2(8), R, __ffma2_rn(W2(6), L, __ffma2_rn(W2(7), v[q], a[q])));
+                    a[q] = __ffma2_rn(W2(5), R, __ffma2_rn(W2(3), L, __ffma2_rn(W2(4), v[q], b[q])));
+                    b[q] = __ffma2_rn(W2(2), R, __ffma2_rn(W2(0), L, __fmul2_rn(W2(1), v[q])));
+                }
+            }
+        } else {
+            const T vl = __shfl_up_sync(0xffffffffu, v[VX - 1], 1);
+            const T vr = __shfl_down_sync(0xffffffffu, v[0], 1);
+#pragma unroll
+            for (int e = 0; e < VX; ++e) {
+                const T L = e == 0 ? vl : v[e - 1];
+                const T R = e == VX - 1 ? vr : v[e + 1];
+                // (terms in v first, the shuffled neighbours L, R last: the
+                // shuffle latency overlaps the first multiply-add)
+                if constexpr (SHAPE == STENCIL_STAR) {
+                    // lambda^(1) dense 3x3, index (dy+1)*3 + (dx+1): N 1, W 3, C 4, E 5, S 7
+                    o[e] = fma(w[7], v[e], a[e]);
+                    a[e] = fma(w[5], R, fma(w[3], L, fma(w[4], v[e], b[e])));
+                    b[e] = w[1] * v[e];
+                } else {
+                    // taps: (dy+1)*3 + (dx+1)
+                    o[e] = fma(w[8], R, fma(w[6], L, fma(w[7], v[e], a[e])));
+                    a[e] = fma(w[5], R, fma(w[3], L, fma(w[4], v[e], b[e])));
+                    b[e] = fma(w[2], R, fma(w[0], L, w[1] * v[e]));
+                }
             }
         }
         const T* srow = ring + sl * C::W + lane * VX;
         if constexpr (CHK) {
-            if ((p->phys_lo && j == -1) || (p->phys_hi && j == p->ny)) tb_lds<T, VX>(o, srow);
+            if ((p->phys_lo && j == -1) || (p->phys_hi && j == p->ny)) tb_lds<NE>(o, srow);
         }
         if constexpr (EDGE) {   // branch-free: no divergence between the shuffles
-            T r[VX];
-            tb_lds<T, VX>(r, srow);
+            E r[NE];
+            tb_lds<NE>(r, srow);
 #pragma unroll
-            for (int e = 0; e < VX; ++e) o[e] = ((rmask >> e) & 1u) ? r[e] : o[e];
+            for (int q = 0; q < NE; ++q) {
+                if constexpr (C::FP2) {   // pair q = columns (q, q + NE)
+                    o[q].x = ((rmask >> q) & 1u) ? r[q].x : o[q].x;
+                    o[q].y = ((rmask >> (q + NE)) & 1u) ? r[q].y : o[q].y;
+                } else {
+                    o[q] = ((rmask >> q) & 1u) ? r[q] : o[q];
+                }
+            }
         }
     }
 
@@ -183,27 +266,27 @@ struct TbWarp {
     // g) outputs row j = i - g - s - 1.  On return v holds the level-K row
     // i - K - (G-1).
     template <bool CHK, bool EDGE>
-    __device__ __forceinline__ void row(const T (&w)[C::NTAP], T (&a)[K][VX], T (&b)[K][VX], T (&pend)[C::G][VX],
-                                        T (&v)[VX], int i, int slot, unsigned rmask) const {
-        T v0[VX];   // the loaded row (v is overwritten by the last group, which runs first)
+    __device__ __forceinline__ void row(const T (&w)[C::NTAP], E (&a)[K][NE], E (&b)[K][NE], E (&pend)[C::G][NE],
+                                        E (&v)[NE], int i, int slot, unsigned rmask) const {
+        E v0[NE];   // the loaded row (v is overwritten by the last group, which runs first)
 #pragma unroll
-        for (int e = 0; e < VX; ++e) v0[e] = v[e];
+        for (int e = 0; e < NE; ++e) v0[e] = v[e];
         constexpr int KG = K / C::G;
 #pragma unroll
         for (int g = C::G - 1; g >= 0; --g) {
-            T x[VX];
+            E x[NE];
 #pragma unroll
-            for (int e = 0; e < VX; ++e) x[e] = g == 0 ? v0[e] : pend[g - 1][e];
+            for (int e = 0; e < NE; ++e) x[e] = g == 0 ? v0[e] : pend[g - 1][e];
 #pragma unroll
             for (int q = 0; q < KG; ++q) {
                 const int s = g * KG + q;
-                T o[VX];
+                E o[NE];
                 stage<CHK, EDGE>(w, a[s], b[s], x, o, i - g - s - 1, (slot - g - s - 1) & (C::D - 1), rmask);
 #pragma unroll
-                for (int e = 0; e < VX; ++e) x[e] = o[e];
+                for (int e = 0; e < NE; ++e) x[e] = o[e];
             }
 #pragma unroll
-            for (int e = 0; e < VX; ++e) {
+            for (int e = 0; e < NE; ++e) {
                 if (g == C::G - 1) v[e] = x[e];
                 else pend[g][e] = x[e];
             }
@@ -242,15 +325,15 @@ struct TbWarp {
             ptx::fence_proxy_async();
             for (int t = 0; t < min(C::PF, nrows); ++t) issue(t);
         }
-        T a[K][VX], b[K][VX], pend[C::G][VX];
+        E a[K][NE], b[K][NE], pend[C::G][NE];
 #pragma unroll
         for (int s = 0; s < K; ++s)
 #pragma unroll
-            for (int e = 0; e < VX; ++e) a[s][e] = b[s][e] = T(0);
+            for (int e = 0; e < NE; ++e) a[s][e] = b[s][e] = E{};
 #pragma unroll
         for (int q = 0; q < C::G; ++q)
 #pragma unroll
-            for (int e = 0; e < VX; ++e) pend[q][e] = T(0);
+            for (int e = 0; e < NE; ++e) pend[q][e] = E{};
         T* g = P.dst + (P.org_y + (long long)(i_lo - C::LAG)) * P.pitch + P.org_x + xl;   // row i - LAG
 #if defined(TB_UNROLL) && TB_UNROLL == 2
 #pragma unroll 2
@@ -265,8 +348,8 @@ struct TbWarp {
             const uint32_t f = f0 + (uint32_t)t;
             const int slot = (int)(f & (C::D - 1));
             ptx::mbar_wait_spin(&bar[slot], (f / C::D) & 1u);
-            T v[VX];
-            tb_lds<T, VX>(v, ring + slot * C::W + lane * VX);
+            E v[NE];
+            tb_lds<NE>(v, ring + slot * C::W + lane * VX);
             const bool chk = i < y0 + C::LAG || (P.phys_hi && i > P.ny);
             bool st = true;
             if (chk) {
@@ -277,11 +360,11 @@ struct TbWarp {
             }
             if (st) {
                 const int j = i - C::LAG;
-                tb_stg<T, VX>(g, v, smask);
+                tb_stg<NE>(g, v, smask);
                 if (P.peer_lo_on && j < P.peer_h)
-                    tb_stg<T, VX>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dlo), v, smask);
+                    tb_stg<NE>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dlo), v, smask);
                 if (P.peer_hi_on && j >= P.ny - P.peer_h)
-                    tb_stg<T, VX>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dhi), v, smask);
+                    tb_stg<NE>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dhi), v, smask);
             }
             g += P.pitch;
         }
