@@ -1208,6 +1208,8 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
         // their shared halo rows are still in L2 (3D halos are ~20% of a tile).
         double share = vol_total > 0 ? double(b.volume()) / double(vol_total) : 1.0;
         int64_t want = std::max<int64_t>(1, (int64_t)(target * share) / std::max<int64_t>(1, cols));
+        if (p->sched_max_ctas > 0)   // (tests) round up: at least 1.5 segments per CTA overall
+            want = std::max<int64_t>(1, ((int64_t)(target * share) + cols - 1) / std::max<int64_t>(1, cols));
         if (C::ND == 3 && cols >= p->sm_count) want = 1;
 #ifdef SB_3D_ZSPLIT
         // (tuning) z-chunks per column; segments are z-chunk-major, so CTAs sweep

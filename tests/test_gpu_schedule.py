@@ -49,7 +49,7 @@ SCHED_CASES = [
 
 
 @pytest.mark.parametrize("dims,shape,dtype,T,m", SCHED_CASES)
-@pytest.mark.parametrize("max_ctas", [16, 0])
+@pytest.mark.parametrize("max_ctas", [10, 0])
 def test_schedule_paths_whole_frame(dims, shape, dtype, T, m, max_ctas):
     nd = len(dims)
     offs = oracle.taps(nd, 1, oracle.STAR if shape == "star" else oracle.BOX)
