@@ -97,11 +97,14 @@ using Cfg2 = Cfg<T, 2, SHAPE, RR, Q, S, (vxm2<SHAPE, Q, RR>() > 1 ? SB_2D_NTXH :
 template <int SHAPE, int Q, int S>
 constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 // (radius-2 3D configs use the defaults: star2_3d is keyed on Q only for r = 1)
+// (round 2: 32x16 consumer threads with 2 rows each instead of 32x8 with 4 --
+// same 64x32 tile and shared memory, 17 instead of 9 warps per SM at 90
+// registers: C4 m=2 571-583 vs 548-557 GStencil/s, 0.71 of HBM, one gpurun call)
 #ifndef SB_S2_NTY
-#define SB_S2_NTY 8
+#define SB_S2_NTY 16
 #endif
 #ifndef SB_S2_VY
-#define SB_S2_VY 4
+#define SB_S2_VY 2
 #endif
 #ifndef SB_S2_PB
 #define SB_S2_PB 2
@@ -121,6 +124,15 @@ constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 #endif
 #ifndef SB_B1_PB
 #define SB_B1_PB 1
+#endif
+// (round 2: 32x16 consumer threads x 4 rows = a 64x64 tile -- y halo 1.06x
+// instead of 1.125x, 17 warps per SM at 92 registers: C5 m=1 367 vs 338
+// GStencil/s, 0.90 of HBM, one gpurun call; 64x32 with 2 rows per thread: 304)
+#ifndef SB_B1_NTY
+#define SB_B1_NTY 16
+#endif
+#ifndef SB_B1_VY
+#define SB_B1_VY 4
 #endif
 template <int SHAPE, int Q, int S, int RR>
 constexpr bool box1_3d() { return SHAPE == STENCIL_BOX && Q == 1 && S == 1 && RR == 1; }
@@ -144,8 +156,9 @@ template <int SHAPE, int Q, int S, int RR>
 constexpr bool box2s_3d() { return SHAPE == STENCIL_BOX && Q == 1 && S == 2 && RR == 1; }
 template <typename T, int SHAPE, int Q, int S, int RR = 1>
 using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32,
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NTY : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NTY : SB_3D_NTY),
-                 (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : box1_3d<SHAPE, Q, S, RR>() ? 4
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_NTY : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NTY
+                                                     : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_NTY : SB_3D_NTY),
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_VY : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_VY
                                                     : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_VY : SB_3D_VY),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_PB : SB_3D_PB),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_NSLOT
