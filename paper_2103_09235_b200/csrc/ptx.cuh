@@ -67,6 +67,50 @@ __device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
     }
 }
 
+// The whole wait loop inside one asm statement (the branch is PTX-level), so
+// the compiler does not wrap it in divergence/reconvergence bookkeeping.
+__device__ __forceinline__ void mbar_wait_loop(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "TB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra TB_WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+
+// Predicated 1-row TMA load: when `pred`, fence the async proxy against
+// earlier generic reads, arm the mbarrier with `bytes` and issue the load
+// (one asm statement, no branch).
+__device__ __forceinline__ void tma_load_2d_pred(bool pred, void* dst, const CUtensorMap* map, uint64_t* bar,
+                                                 uint32_t bytes, int x, int y) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.u32 p, %0, 0;\n\t"
+        "@p fence.proxy.async.shared::cta;\n\t"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n\t"
+        "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%3], [%4, {%5, %6}], [%1];\n\t}" ::"r"((uint32_t)pred),
+        "r"(smem_u32(bar)), "r"(bytes), "r"(smem_u32(dst)), "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y)
+        : "memory");
+}
+
+// Predicated 16-byte global stores.
+__device__ __forceinline__ void stg_v2_pred(bool pred, double* g, double a, double b) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+        "@p st.global.v2.f64 [%1], {%2, %3};\n\t}" ::"r"((uint32_t)pred),
+        "l"(g), "d"(a), "d"(b)
+        : "memory");
+}
+__device__ __forceinline__ void stg_v4_pred(bool pred, float* g, float a, float b, float c, float d) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+        "@p st.global.v4.f32 [%1], {%2, %3, %4, %5};\n\t}" ::"r"((uint32_t)pred),
+        "l"(g), "f"(a), "f"(b), "f"(c), "f"(d)
+        : "memory");
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     while (!mbar_try_wait(bar, parity)) {
     }

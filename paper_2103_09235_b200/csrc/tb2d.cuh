@@ -117,6 +117,22 @@ __device__ __forceinline__ void tb_lds(T (&v)[VX], const T* s) {
     }
 }
 
+// Non-edge units: every 16-byte vector of a lane is either fully stored or not
+// (aligned output range), so each is one predicated vector store, no branch.
+template <int VX, typename T>
+__device__ __forceinline__ void tb_stg_aligned(T* g, const T (&v)[VX], unsigned mask) {
+    constexpr int EV = 16 / (int)sizeof(T);
+#pragma unroll
+    for (int q = 0; q < VX / EV; ++q) {
+        const bool on = (mask >> (q * EV)) & 1u;
+        if constexpr (sizeof(T) == 8)
+            ptx::stg_v2_pred(on, reinterpret_cast<double*>(g) + 2 * q, v[2 * q], v[2 * q + 1]);
+        else
+            ptx::stg_v4_pred(on, reinterpret_cast<float*>(g) + 4 * q, v[4 * q], v[4 * q + 1], v[4 * q + 2],
+                             v[4 * q + 3]);
+    }
+}
+
 template <int VX, typename T>
 __device__ __forceinline__ void tb_stg(T* g, const T (&v)[VX], unsigned mask) {
     constexpr int EV = 16 / (int)sizeof(T);   // elements per 16-byte vector
@@ -301,7 +317,8 @@ struct TbWarp {
         const int nrows = i_end - i_lo + 1;
         const int xl = x0 + lane * VX;
         // stores: every valid output of the window (overlapping strips write identical values)
-        const int vlo = max(x0 + K, 0), vhi = min(x0 + C::W - K, P.nx);
+        // (non-edge strips store the aligned middle [x0 + KA, x0 + W - KA): whole vectors)
+        const int vlo = EDGE ? max(x0 + K, 0) : x0 + C::KA, vhi = EDGE ? min(x0 + C::W - K, P.nx) : x0 + C::W - C::KA;
         unsigned smask = 0;
 #pragma unroll
         for (int e = 0; e < VX; ++e)
@@ -319,6 +336,13 @@ struct TbWarp {
             const int yr = min(i_lo + t, ymax);        // rows past the allocation: any row (never valid)
             ptx::mbar_expect_tx(&bar[sl], C::ROW_BYTES);
             ptx::tma_load_2d(ring + sl * C::W, tmap, &bar[sl], (int)P.org_x + x0, (int)P.org_y + yr);
+        };
+        auto issue_pred = [&](bool pred, int t) {      // (steady state: no branch)
+            const uint32_t f = f0 + (uint32_t)t;
+            const int sl = (int)(f & (C::D - 1));
+            const int yr = min(i_lo + t, ymax);
+            ptx::tma_load_2d_pred(pred, ring + sl * C::W, tmap, &bar[sl], C::ROW_BYTES, (int)P.org_x + x0,
+                                  (int)P.org_y + yr);
         };
         __syncwarp();
         if (lane == 0) {
@@ -341,13 +365,10 @@ struct TbWarp {
         for (int t = 0; t < nrows; ++t) {
             const int i = i_lo + t;
             __syncwarp();
-            if (lane == 0 && t + C::PF < nrows) {
-                ptx::fence_proxy_async();
-                issue(t + C::PF);
-            }
+            issue_pred(lane == 0 && t + C::PF < nrows, t + C::PF);
             const uint32_t f = f0 + (uint32_t)t;
             const int slot = (int)(f & (C::D - 1));
-            ptx::mbar_wait_spin(&bar[slot], (f / C::D) & 1u);
+            ptx::mbar_wait_loop(&bar[slot], (f / C::D) & 1u);
             E v[NE];
             tb_lds<NE>(v, ring + slot * C::W + lane * VX);
             const bool chk = i < y0 + C::LAG || (P.phys_hi && i > P.ny);
@@ -360,11 +381,13 @@ struct TbWarp {
             }
             if (st) {
                 const int j = i - C::LAG;
-                tb_stg<NE>(g, v, smask);
-                if (P.peer_lo_on && j < P.peer_h)
-                    tb_stg<NE>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dlo), v, smask);
-                if (P.peer_hi_on && j >= P.ny - P.peer_h)
-                    tb_stg<NE>(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dhi), v, smask);
+                auto put = [&](T* dst) {
+                    if constexpr (EDGE || C::FP2) tb_stg<NE>(dst, v, smask);
+                    else tb_stg_aligned<NE>(dst, v, smask);
+                };
+                put(g);
+                if (P.peer_lo_on && j < P.peer_h) put(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dlo));
+                if (P.peer_hi_on && j >= P.ny - P.peer_h) put(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dhi));
             }
             g += P.pitch;
         }
