@@ -79,15 +79,16 @@ __device__ __forceinline__ void mbar_wait_loop(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// Predicated 1-row TMA load: when `pred`, fence the async proxy against
-// earlier generic reads, arm the mbarrier with `bytes` and issue the load
-// (one asm statement, no branch).
+// Predicated 1-row TMA load: when `pred`, arm the mbarrier with `bytes` and
+// issue the load (one asm statement).  No proxy fence: the slot's earlier
+// generic accesses are reads, completed iterations ago (a WAR on the slot, as
+// in a TMA pipeline's consumer-release / producer-acquire; a fence here
+// compiled to MEMBAR.ALL.CTA, which waited for this lane's global stores).
 __device__ __forceinline__ void tma_load_2d_pred(bool pred, void* dst, const CUtensorMap* map, uint64_t* bar,
                                                  uint32_t bytes, int x, int y) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "setp.ne.u32 p, %0, 0;\n\t"
-        "@p fence.proxy.async.shared::cta;\n\t"
         "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n\t"
         "@p cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
         " [%3], [%4, {%5, %6}], [%1];\n\t}" ::"r"((uint32_t)pred),
