@@ -359,10 +359,11 @@ struct TbWarp {
 #pragma unroll
             for (int e = 0; e < NE; ++e) pend[q][e] = E{};
         T* g = P.dst + (P.org_y + (long long)(i_lo - C::LAG)) * P.pitch + P.org_x + xl;   // row i - LAG
-#if defined(TB_UNROLL) && TB_UNROLL == 2
-#pragma unroll 2
-#endif
-        for (int t = 0; t < nrows; ++t) {
+        // One iteration: load row i = i_lo + t, K stages, store row i - LAG.
+        // CHK iterations may output a ring row, a row outside [y0, y1) or a row
+        // with peer stores; the steady middle runs without any of those tests.
+        auto body = [&](auto chk_tag, int t) {
+            constexpr bool CHK = decltype(chk_tag)::value;
             const int i = i_lo + t;
             __syncwarp();
             issue_pred(lane == 0 && t + C::PF < nrows, t + C::PF);
@@ -371,26 +372,36 @@ struct TbWarp {
             ptx::mbar_wait_loop(&bar[slot], (f / C::D) & 1u);
             E v[NE];
             tb_lds<NE>(v, ring + slot * C::W + lane * VX);
-            const bool chk = i < y0 + C::LAG || (P.phys_hi && i > P.ny);
-            bool st = true;
-            if (chk) {
-                row<true, EDGE>(w, a, b, pend, v, i, slot, rmask);
-                st = i - C::LAG >= y0 && i - C::LAG < y1;
-            } else {
-                row<false, EDGE>(w, a, b, pend, v, i, slot, rmask);
-            }
-            if (st) {
+            row<CHK, EDGE>(w, a, b, pend, v, i, slot, rmask);
+            T* gi = g + (long long)t * P.pitch;
+            auto put = [&](T* dst) {
+                if constexpr (EDGE || C::FP2) tb_stg<NE>(dst, v, smask);
+                else tb_stg_aligned<NE>(dst, v, smask);
+            };
+            if constexpr (CHK) {
                 const int j = i - C::LAG;
-                auto put = [&](T* dst) {
-                    if constexpr (EDGE || C::FP2) tb_stg<NE>(dst, v, smask);
-                    else tb_stg_aligned<NE>(dst, v, smask);
-                };
-                put(g);
-                if (P.peer_lo_on && j < P.peer_h) put(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dlo));
-                if (P.peer_hi_on && j >= P.ny - P.peer_h) put(reinterpret_cast<T*>(reinterpret_cast<char*>(g) + P.peer_dhi));
+                if (j >= y0 && j < y1) {
+                    put(gi);
+                    if (P.peer_lo_on && j < P.peer_h) put(reinterpret_cast<T*>(reinterpret_cast<char*>(gi) + P.peer_dlo));
+                    if (P.peer_hi_on && j >= P.ny - P.peer_h)
+                        put(reinterpret_cast<T*>(reinterpret_cast<char*>(gi) + P.peer_dhi));
+                }
+            } else {
+                put(gi);
             }
-            g += P.pitch;
-        }
+        };
+        // steady iterations: i >= y0 + LAG (stores start, no top ring row), no
+        // bottom ring row (i <= ny when phys_hi), no peer rows
+        int t_lo = y0 + C::LAG - i_lo;
+        if (P.peer_lo_on) t_lo = max(t_lo, P.peer_h + C::LAG - i_lo);
+        int t_hi = nrows;                                           // exclusive
+        if (P.phys_hi) t_hi = min(t_hi, P.ny + 1 - i_lo);
+        if (P.peer_hi_on) t_hi = min(t_hi, P.ny - P.peer_h + C::LAG - i_lo);
+        t_lo = min(max(t_lo, 0), nrows);
+        t_hi = max(t_hi, t_lo);
+        for (int t = 0; t < t_lo; ++t) body(std::true_type{}, t);
+        for (int t = t_lo; t < t_hi; ++t) body(std::false_type{}, t);
+        for (int t = t_hi; t < nrows; ++t) body(std::true_type{}, t);
         fill = f0 + (uint32_t)nrows;
     }
 };
