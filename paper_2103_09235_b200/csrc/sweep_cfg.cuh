@@ -115,6 +115,12 @@ constexpr bool star2_3d() { return SHAPE == STENCIL_STAR && Q == 2 && S == 1; }
 #ifndef SB_S2_MINB
 #define SB_S2_MINB 1
 #endif
+// (round 2: 128-column tiles -- SB_S2_VXM=2 with 12x2 or 8x2 rows per thread
+// group -- cut the DRAM reads only from 1.41 to 1.35 GB per sweep and ran at
+// 365-469 vs 563 GStencil/s: fewer resident warps; one gpurun call)
+#ifndef SB_S2_VXM
+#define SB_S2_VXM 1     // 16-byte vectors of x outputs per thread
+#endif
 // The single 3D box step (27 taps, C5 m=1) takes 4 output rows per thread in a
 // 64x32 tile with 3 one-plane slots, 1 CTA/SM (measured 346 vs 318 GStencil/s
 // in one gpurun call; the same change costs 14% on the 7-tap star, which keeps
@@ -162,7 +168,8 @@ using Cfg3 = Cfg<T, 3, SHAPE, RR, Q, S, 32,
                                                     : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_VY : SB_3D_VY),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_PB : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_PB : SB_3D_PB),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_NSLOT : box1_3d<SHAPE, Q, S, RR>() ? SB_B1_NSLOT
-                                                       : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NSLOT : SB_3D_NSLOT), 1,
+                                                       : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_NSLOT : SB_3D_NSLOT),
+                 (star2_3d<SHAPE, Q, S>() ? SB_S2_VXM : 1),
                  (star2_3d<SHAPE, Q, S>() ? SB_S2_MINB : box1_3d<SHAPE, Q, S, RR>() ? 1
                                                       : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_MINB : SB_3D_MINB),
                  SB_ROT_3D, (star2_3d<SHAPE, Q, S>() ? 1 : box2s_3d<SHAPE, Q, S, RR>() ? SB_B2_PINC : SB_PINC_3D)>;

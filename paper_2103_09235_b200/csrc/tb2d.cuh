@@ -71,6 +71,9 @@ constexpr int TB_D = 16;   // shared row slots per warp (power of two)
 #ifndef TB_FFMA2
 #define TB_FFMA2 0         // fp32 element pairs with packed FFMA2: measured slower
 #endif
+#ifndef TB_LOAD_AHEAD
+#define TB_LOAD_AHEAD -1   // read row t+1 from its slot after computing row t (-1: for K = 8)
+#endif
 
 template <typename T, int SHAPE, int K, int VX, int NW>
 struct TbCfg {
@@ -93,6 +96,9 @@ struct TbCfg {
     static constexpr bool FP2 = sizeof(T) == 4 && TB_FFMA2;
     using E = std::conditional_t<FP2, float2, T>;
     static constexpr int NE = FP2 ? VX / 2 : VX;   // elements per lane
+    // load-ahead (measured, one call: C2 K=8 1909 vs 1864, C3 K=8 2754 vs 2697,
+    // C2 K=6 1858 vs 1882 GStencil/s): on for the deepest block only
+    static constexpr bool LA = TB_LOAD_AHEAD < 0 ? K >= 8 : TB_LOAD_AHEAD != 0;
     static_assert(K >= 1 && PF >= 2, "temporal block too deep for the slot ring");
     static_assert(W <= 256, "TMA box dimension");
     static_assert((VX * sizeof(T)) % 16 == 0, "16-byte lane vectors");
@@ -362,6 +368,20 @@ struct TbWarp {
         // One iteration: load row i = i_lo + t, K stages, store row i - LAG.
         // CHK iterations may output a ring row, a row outside [y0, y1) or a row
         // with peer stores; the steady middle runs without any of those tests.
+        // Load-ahead (C::LA): row t+1 is waited for and read from its slot right
+        // after the K stages of row t, so its shared-memory latency overlaps the
+        // tail of row t's multiply-adds and stores instead of stalling the
+        // first multiply-adds of the next iteration.
+        E vin[NE];
+        auto fetch = [&](int t) {
+            const uint32_t f = f0 + (uint32_t)t;
+            const int sl = (int)(f & (C::D - 1));
+            ptx::mbar_wait_loop(&bar[sl], (f / C::D) & 1u);
+            tb_lds<NE>(vin, ring + sl * C::W + lane * VX);
+        };
+        if constexpr (C::LA) {
+            if (nrows > 0) fetch(0);
+        }
         auto body = [&](auto chk_tag, int t) {
             constexpr bool CHK = decltype(chk_tag)::value;
             const int i = i_lo + t;
@@ -369,10 +389,17 @@ struct TbWarp {
             issue_pred(lane == 0 && t + C::PF < nrows, t + C::PF);
             const uint32_t f = f0 + (uint32_t)t;
             const int slot = (int)(f & (C::D - 1));
-            ptx::mbar_wait_loop(&bar[slot], (f / C::D) & 1u);
             E v[NE];
-            tb_lds<NE>(v, ring + slot * C::W + lane * VX);
-            row<CHK, EDGE>(w, a, b, pend, v, i, slot, rmask);
+            if constexpr (C::LA) {
+#pragma unroll
+                for (int e = 0; e < NE; ++e) v[e] = vin[e];
+                row<CHK, EDGE>(w, a, b, pend, v, i, slot, rmask);
+                if (!CHK || t + 1 < nrows) fetch(t + 1);   // (steady iterations end before nrows - 1)
+            } else {
+                ptx::mbar_wait_loop(&bar[slot], (f / C::D) & 1u);
+                tb_lds<NE>(v, ring + slot * C::W + lane * VX);
+                row<CHK, EDGE>(w, a, b, pend, v, i, slot, rmask);
+            }
             T* gi = g + (long long)t * P.pitch;
             auto put = [&](T* dst) {
                 if constexpr (EDGE || C::FP2) tb_stg<NE>(dst, v, smask);
@@ -397,6 +424,7 @@ struct TbWarp {
         int t_hi = nrows;                                           // exclusive
         if (P.phys_hi) t_hi = min(t_hi, P.ny + 1 - i_lo);
         if (P.peer_hi_on) t_hi = min(t_hi, P.ny - P.peer_h + C::LAG - i_lo);
+        if constexpr (C::LA) t_hi = min(t_hi, nrows - 1);          // the last row fetches nothing
         t_lo = min(max(t_lo, 0), nrows);
         t_hi = max(t_hi, t_lo);
         for (int t = 0; t < t_lo; ++t) body(std::true_type{}, t);
