@@ -71,6 +71,12 @@ constexpr int TB_D = 16;   // shared row slots per warp (power of two)
 #ifndef TB_FFMA2
 #define TB_FFMA2 0         // fp32 element pairs with packed FFMA2: measured slower
 #endif
+#ifndef TB_ISSUE_LATE
+#define TB_ISSUE_LATE -1   // issue the next rows' TMA after the stages (-1: for fp64)
+#endif
+#ifndef TB_NB
+#define TB_NB 1            // steady-state TMA rows per issue sequence
+#endif
 #ifndef TB_LOAD_AHEAD
 #define TB_LOAD_AHEAD -1   // read row t+1 from its slot after computing row t (-1: for K = 8)
 #endif
@@ -99,6 +105,10 @@ struct TbCfg {
     // load-ahead (measured, one call: C2 K=8 1909 vs 1864, C3 K=8 2754 vs 2697,
     // C2 K=6 1858 vs 1882 GStencil/s): on for the deepest block only
     static constexpr bool LA = TB_LOAD_AHEAD < 0 ? K >= 8 : TB_LOAD_AHEAD != 0;
+    // late issue (measured, one call: C2 K=8 1960 vs 1917, K=6 1959 vs 1879;
+    // C3 f32 K=8 2660 vs 2755 GStencil/s): fp64 only
+    static constexpr bool IL = TB_ISSUE_LATE < 0 ? sizeof(T) == 8 : TB_ISSUE_LATE != 0;
+    static constexpr int NB = TB_NB;
     static_assert(K >= 1 && PF >= 2, "temporal block too deep for the slot ring");
     static_assert(W <= 256, "TMA box dimension");
     static_assert((VX * sizeof(T)) % 16 == 0, "16-byte lane vectors");
@@ -382,11 +392,30 @@ struct TbWarp {
         if constexpr (C::LA) {
             if (nrows > 0) fetch(0);
         }
-        auto body = [&](auto chk_tag, int t) {
+        // TMA issue: rows [nis, t + PF] (at most NI of them) from lane 0.  The
+        // head iterations issue one row each; the steady loop issues a batch
+        // of C::NB rows every C::NB iterations (fewer issue sequences per row;
+        // the prefetch depth then varies between PF - NB + 1 and PF rows).
+        // (Every row t + 1 is issued before iteration t fetches it and no slot
+        // is refilled while a row in it can still be read: checked for all
+        // loop splits with a host simulation of this schedule.)
+        int nis = min(C::PF, nrows);
+        auto issue_rows = [&](auto ni_tag, int t) {
+            constexpr int NI = decltype(ni_tag)::value;
+            if constexpr (NI > 0) {
+                __syncwarp();
+#pragma unroll
+                for (int k = 0; k < NI; ++k) {
+                    const int r = nis + k;
+                    issue_pred(lane == 0 && r <= t + C::PF && r < nrows, r);
+                }
+                nis = min(nis + NI, t + C::PF + 1);   // (rows [nis, t + PF] issued, at most NI)
+            }
+        };
+        auto body = [&](auto chk_tag, auto ni_tag, int t) {
             constexpr bool CHK = decltype(chk_tag)::value;
             const int i = i_lo + t;
-            __syncwarp();
-            issue_pred(lane == 0 && t + C::PF < nrows, t + C::PF);
+            if constexpr (!C::IL) issue_rows(ni_tag, t);
             const uint32_t f = f0 + (uint32_t)t;
             const int slot = (int)(f & (C::D - 1));
             E v[NE];
@@ -394,11 +423,13 @@ struct TbWarp {
 #pragma unroll
                 for (int e = 0; e < NE; ++e) v[e] = vin[e];
                 row<CHK, EDGE>(w, a, b, pend, v, i, slot, rmask);
+                if constexpr (C::IL) issue_rows(ni_tag, t);
                 if (!CHK || t + 1 < nrows) fetch(t + 1);   // (steady iterations end before nrows - 1)
             } else {
                 ptx::mbar_wait_loop(&bar[slot], (f / C::D) & 1u);
                 tb_lds<NE>(v, ring + slot * C::W + lane * VX);
                 row<CHK, EDGE>(w, a, b, pend, v, i, slot, rmask);
+                if constexpr (C::IL) issue_rows(ni_tag, t);
             }
             T* gi = g + (long long)t * P.pitch;
             auto put = [&](T* dst) {
@@ -417,6 +448,9 @@ struct TbWarp {
                 put(gi);
             }
         };
+        using one = std::integral_constant<int, 1>;
+        using none = std::integral_constant<int, 0>;
+        using batch = std::integral_constant<int, C::NB>;
         // steady iterations: i >= y0 + LAG (stores start, no top ring row), no
         // bottom ring row (i <= ny when phys_hi), no peer rows
         int t_lo = y0 + C::LAG - i_lo;
@@ -427,9 +461,18 @@ struct TbWarp {
         if constexpr (C::LA) t_hi = min(t_hi, nrows - 1);          // the last row fetches nothing
         t_lo = min(max(t_lo, 0), nrows);
         t_hi = max(t_hi, t_lo);
-        for (int t = 0; t < t_lo; ++t) body(std::true_type{}, t);
-        for (int t = t_lo; t < t_hi; ++t) body(std::false_type{}, t);
-        for (int t = t_hi; t < nrows; ++t) body(std::true_type{}, t);
+        for (int t = 0; t < t_lo; ++t) body(std::true_type{}, one{}, t);
+        int t = t_lo;
+        if constexpr (C::NB > 1) {
+            for (; t + C::NB <= t_hi; t += C::NB) {
+                body(std::false_type{}, batch{}, t);
+#pragma unroll
+                for (int k = 1; k < C::NB; ++k) body(std::false_type{}, none{}, t + k);
+            }
+        }
+        // (the remainder and the tail issue up to NB rows: they catch up after a batch)
+        for (; t < t_hi; ++t) body(std::false_type{}, batch{}, t);
+        for (int t2 = t_hi; t2 < nrows; ++t2) body(std::true_type{}, batch{}, t2);
         fill = f0 + (uint32_t)nrows;
     }
 };

@@ -10,11 +10,21 @@ namespace sb {
 #ifndef TB_NW
 #define TB_NW 8
 #endif
+#ifndef TB_NW_AUTO
+#define TB_NW_AUTO 0
+#endif
+// resident one-warp CTAs per SM for a block of K steps: 8 (TB_NW), or with
+// TB_NW_AUTO the register file's limit for K's register count (measured, one
+// call: 12 warps at K <= 5, 10 at K = 6 -- which the per-SMSP register file
+// caps at 168 registers, 3 warps per sub-partition -- run C2 K=4/5/6 at
+// 1196/1530/1670 vs 1312/1780/1947 GStencil/s with 8; C3 K=4 2528 vs 2462,
+// K=6 2129 vs 2520: kept at 8)
+constexpr int tb_nw(int K) { return TB_NW_AUTO ? (K <= 5 ? 12 : K == 6 ? 10 : K == 7 ? 9 : 8) : TB_NW; }
 
 template <int SHAPE, int... Ks>
 static TbLaunchFn pick_k(int K, std::integer_sequence<int, Ks...>) {
     TbLaunchFn fn = nullptr;
-    ((K == Ks + 2 ? (fn = tb2d_launch<float, SHAPE, Ks + 2, TB_F32_VX, TB_NW>, 0) : 0), ...);
+    ((K == Ks + 2 ? (fn = tb2d_launch<float, SHAPE, Ks + 2, TB_F32_VX, tb_nw(Ks + 2)>, 0) : 0), ...);
     return fn;
 }
 

@@ -4,7 +4,7 @@
 pass=a; if [ "$1" = -p ]; then pass=$2; shift 2; fi
 for name in "$@"; do
   if [ "$name" = main ]; then unset STENCIL_B200_LIB; else export STENCIL_B200_LIB=tunelibs/lib_$name.so; fi
-  for cfg in "c2 8" "c3 8" "c2 6"; do set -- $cfg
+  for cfg in ${TB_CFGS:-"c2 8" "c3 8" "c2 6"}; do set -- ${cfg/:/ }
     timeout 120 python bench.py --config $1 --fold-m $2 --stages $2 --steps 5 --headline-only --no-cpu-baseline > gpurun_out/tt_${name}_$1_k$2_$pass.json 2>gpurun_out/tt_${name}_$1_k$2_$pass.err
   done
 done
