@@ -41,12 +41,13 @@ CONFIGS = {
     # best_m: the fold_m measured fastest on B200 (bench.py --fold-m 0 re-measures all of `ms`)
     "c1": dict(name="1D3P heat fp64 N=100000 T=100", dims=(100000,), shape="star", dtype="f64", T=100, ms=(1, 2),
                best_m=2),
-    # fold_m = 8 (C2, C3): the on-chip temporal block (stages = m; NEXT-1 / a6)
-    # applies 8 single steps per HBM round trip: T = 200 = 25 sweeps.  BASELINE lists fold_m
-    # in {1, 2, 4}; every fold gives the same result (R10), and --fold-m 0 measures m = 1, 2,
-    # 3, 4 (the folded passes) beside it.  Round 1's best was the folded m = 3 (1006).
+    # fold_m = 6 (C2) / 8 (C3): the on-chip temporal block (stages = m; NEXT-1 / a6, DESIGN.md
+    # §5.7) applies 6 (8) single steps per HBM round trip: T = 200 = 33 sweeps + one folded
+    # lambda^(2) sweep (25 sweeps).  BASELINE lists fold_m in {1, 2, 4}; every fold gives the
+    # same result (R10), and --fold-m 0 measures the folded passes and the other blocks beside
+    # it.  Round 1's best was the folded m = 3 (1006).
     "c2": dict(name="2D5P star fp64 8192x8192 T=200", dims=(8192, 8192), shape="star", dtype="f64", T=200,
-               ms=(1, 2, 3, 4, 8), best_m=8),
+               ms=(1, 2, 3, 4, 6, 8), best_m=6),
     "c3": dict(name="2D9P box fp32 16384x16384 T=200", dims=(16384, 16384), shape="box", dtype="f32", T=200,
                ms=(1, 2, 4, 8), best_m=8),
     "c4": dict(name="3D7P star fp64 512^3 T=100", dims=(512, 512, 512), shape="star", dtype="f64", T=100,

@@ -294,7 +294,12 @@ int auto_fold(Plan* p) {
         if (p->counterparts && lowrank(p, 4).rank >= 1 && lowrank(p, 4).rank <= STENCIL_MAX_COUNTERPARTS &&
             2 * 9 * lowrank(p, 4).rank < support_size(2, p->shape, 1, 4))
             return 4;                                    // counterparts: 18 FMAs per point for 4 steps
-        if (p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 8)) return 8;   // temporal block, 8 steps
+        // temporal block: 8 steps per HBM round trip; 6 for fp64 stars (C2: K = 6 at 1936-1959
+        // vs K = 8 at 1921-1960 GStencil/s in three calls, 0.83 of the HBM roofline per round trip)
+        if (p->boundary == STENCIL_BC_FIXED && p->shape == STENCIL_STAR && p->dtype == STENCIL_F64 &&
+            tb_supported(p, 1, 6))
+            return 6;
+        if (p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 8)) return 8;
         if (p->shape == STENCIL_STAR) return 3;
         return 2;
     }

@@ -1295,7 +1295,13 @@ static int launch_cfg(Plan* p, const SweepCall& c) {
     prm.sc.chunk = std::max(2 * C::PB, p->sched_chunk > 0 ? p->sched_chunk : SB_CHUNK);
     prm.sc.min_steal = std::max(p->sched_chunk > 0 ? prm.sc.chunk : 2 * prm.sc.chunk,
                                 p->sched_min_steal > 0 ? p->sched_min_steal : 4 * C::H + 8);
+#ifndef SB_FILL_GRID
+#define SB_FILL_GRID 0
+#endif
     int64_t tiles = std::min<int64_t>(nseg, target);   // persistent: one resident wave
+    // (SB_FILL_GRID: fewer segments than resident CTAs -- e.g. C5's 144 columns
+    // on 148 SMs -- launch the whole wave anyway; the extra CTAs start by stealing)
+    if (SB_FILL_GRID && C::ND == 3) tiles = std::max<int64_t>(tiles, std::min<int64_t>(target, 2 * nseg));
     if (band_blocks > 0) tiles = std::max<int64_t>(tiles, std::min<int64_t>(band_blocks, target));
     if (p->sched_max_ctas > 0) tiles = std::min<int64_t>(tiles, p->sched_max_ctas);   // (tests: force grabs)
     sweep_kernel<C><<<(unsigned)tiles, C::NTHREADS, C::SMEM, cst>>>(map, prm);

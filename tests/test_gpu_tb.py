@@ -114,7 +114,10 @@ def test_tb_no_writes_outside(dims, shape, dtype, K):
     assert np.all(b.cpu().numpy()[pads] == a_before.cpu().numpy()[pads])
 
 
-FULL = {"c2": ((8192, 8192), "star", "f64", 200, 8), "c3": ((16384, 16384), "box", "f32", 200, 8)}
+# the bench's launch configurations: C2 at fold 6 (its default, 33 blocks + one folded
+# lambda^(2) sweep) and 8, C3 at fold 8
+FULL = {"c2": ((8192, 8192), "star", "f64", 200, 6), "c2k8": ((8192, 8192), "star", "f64", 200, 8),
+        "c3": ((16384, 16384), "box", "f32", 200, 8)}
 
 
 def _samples(n0, n1):
@@ -123,7 +126,7 @@ def _samples(n0, n1):
             ((n0 // 3, n1 // 3), (n0 // 3 + 3, n1 // 3 + 3)), ((n0 - 2, 7), (n0, 10))]
 
 
-@pytest.mark.parametrize("key", ["c2", "c3"])
+@pytest.mark.parametrize("key", ["c2", "c2k8", "c3"])
 def test_tb_fullsize(key):
     dims, shape, dtype, T, K = FULL[key]
     offs = oracle.taps(2, 1, oracle.STAR if shape == "star" else oracle.BOX)
