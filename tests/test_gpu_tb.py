@@ -69,12 +69,13 @@ def test_tb_dyadic_bitwise(K, shape, dims, T):
 
 
 @pytest.mark.parametrize("exchange", ["copies", "peer"])
-@pytest.mark.parametrize("dims,shape,dtype,K,G", [((64, 700), "star", "f64", 4, 4), ((96, 1100), "box", "f32", 8, 3),
-                                                  ((48, 300), "star", "f64", 8, 2)])
-def test_tb_dist_emulated_bitwise(exchange, dims, shape, dtype, K, G):
+@pytest.mark.parametrize("dims,shape,dtype,K,G,T", [((64, 700), "star", "f64", 4, 4, 9), ((96, 1100), "box", "f32", 8, 3, 17),
+                                                    ((48, 300), "star", "f64", 8, 2, 17),
+                                                    # the bench's N > 1 configuration: fold 6 with T mod 6 = 2
+                                                    ((72, 1030), "star", "f64", 6, 3, 20)])
+def test_tb_dist_emulated_bitwise(exchange, dims, shape, dtype, K, G, T):
     k = len(oracle.taps(2, 1, oracle.STAR if shape == "star" else oracle.BOX))
     plan = _plan(dims, shape, dtype, synth.weights(k, 1))
-    T = 2 * K + 1
     a, b, ws = plan.empty(), plan.empty(), plan.empty()
     plan.fill_random(a, 2)
     plan.run(a, b, T, K, workspace=ws, stages=K)
