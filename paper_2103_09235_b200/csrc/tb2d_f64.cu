@@ -34,6 +34,10 @@ namespace sb {
 #ifndef TB_F64_VX
 #define TB_F64_VX 4
 #endif
+#ifndef TB_F64_VX6
+#define TB_F64_VX6 4       // doubles per lane for blocks of K <= 6 steps (6: measured slower)
+#endif
+constexpr int tb_vx64(int K) { return K <= 6 ? TB_F64_VX6 : TB_F64_VX; }
 #ifndef TB_NW
 #define TB_NW 8
 #endif
@@ -51,7 +55,7 @@ constexpr int tb_nw(int K) { return TB_NW_AUTO ? (K <= 5 ? 12 : K == 6 ? 10 : K 
 template <int SHAPE, int... Ks>
 static TbLaunchFn pick_k(int K, std::integer_sequence<int, Ks...>) {
     TbLaunchFn fn = nullptr;
-    ((K == Ks + 2 ? (fn = tb2d_launch<double, SHAPE, Ks + 2, TB_F64_VX, tb_nw(Ks + 2)>, 0) : 0), ...);
+    ((K == Ks + 2 ? (fn = tb2d_launch<double, SHAPE, Ks + 2, tb_vx64(Ks + 2), tb_nw(Ks + 2)>, 0) : 0), ...);
     return fn;
 }
 
