@@ -50,8 +50,11 @@ CONFIGS = {
                ms=(1, 2, 3, 4, 6, 8), best_m=6),
     "c3": dict(name="2D9P box fp32 16384x16384 T=200", dims=(16384, 16384), shape="box", dtype="f32", T=200,
                ms=(1, 2, 4, 8), best_m=8),
+    # fold_m = 4 (C4): the 3D temporal block (tb3d), 4 single steps per HBM
+    # round trip, T = 100 = 25 sweeps; --fold-m 0 also measures the folded m = 1, 2 passes and
+    # the block at m = 3.
     "c4": dict(name="3D7P star fp64 512^3 T=100", dims=(512, 512, 512), shape="star", dtype="f64", T=100,
-               ms=(1, 2), best_m=2),
+               ms=(1, 2, 3, 4), best_m=4),
     "c5": dict(name="3D27P box fp64 768x768x384 T=100", dims=(384, 768, 768), shape="box", dtype="f64", T=100,
                ms=(1, 2), best_m=1),
     # not a BASELINE config: C3's domain with the UNIFORM 2D9P weights of the paper's

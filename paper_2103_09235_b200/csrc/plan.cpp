@@ -182,6 +182,12 @@ Variant choose_variant(Plan* p, int m) {
     if (p->ndim == 2 && p->r == 1 && p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, m) &&
         (m >= 4 || (m == 3 && p->shape == STENCIL_BOX)))
         return {1, m};
+    // 3D radius-1 fp64 FIXED stars: the CTA-tile temporal block (tb3d.cuh, m single steps
+    // per HBM round trip) beats one folded pass from m = 3 on -- measured on B200 (DESIGN.md
+    // §5.8: C4 m=4 624 vs the folded m=2 571 GStencil/s; K=2 520)
+    if (p->ndim == 3 && p->r == 1 && p->boundary == STENCIL_BC_FIXED && p->shape == STENCIL_STAR &&
+        tb_supported(p, 1, m) && m >= 3)
+        return {1, m};
     if (full <= 64) return {m, 1};
     Variant best = {m, 1};
     double best_cost = 1e30;
@@ -303,7 +309,10 @@ int auto_fold(Plan* p) {
         if (p->shape == STENCIL_STAR) return 3;
         return 2;
     }
-    if (p->ndim == 3 && p->r == 1) return p->shape == STENCIL_STAR ? 2 : 1;
+    if (p->ndim == 3 && p->r == 1) {
+        if (p->shape == STENCIL_STAR && p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 4)) return 4;   // tb3d
+        return p->shape == STENCIL_STAR ? 2 : 1;
+    }
     return 1;
 }
 

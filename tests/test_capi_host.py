@@ -222,5 +222,8 @@ def test_auto_fold_table():
     bx = Plan((64, 64), 1, "box", synth.weights(9, 1), dtype="f32")
     assert st.variant(3) == (3, 1, 0) and st.variant(4) == (1, 4, 0) and st.variant(8) == (1, 8, 0)
     assert bx.variant(2) == (2, 1, 0) and bx.variant(3) == (1, 3, 0)
-    assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1)).auto_fold() == 2
+    assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1)).auto_fold() == 4          # temporal block (tb3d)
+    assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1), dtype="f32").auto_fold() == 2
+    s3 = Plan((16, 16, 16), 1, "star", synth.weights(7, 1))
+    assert s3.variant(2) == (2, 1, 0) and s3.variant(3) == (1, 3, 0) and s3.variant(4) == (1, 4, 0)
     assert Plan((16, 16, 16), 1, "box", synth.weights(27, 1)).auto_fold() == 1

@@ -21,7 +21,7 @@ def main():
     B.build()
     out = os.path.join(ROOT, "tunelibs")
     os.makedirs(out, exist_ok=True)
-    tuned = [f for f in B.SOURCES if f.startswith(("sweep", "tb2d")) or f in ("run.cu", "aux.cu")]
+    tuned = [f for f in B.SOURCES if f.startswith(("sweep", "tb2d", "tb3d")) or f in ("run.cu", "aux.cu")]
     defs = ["-DSTENCIL_TUNING_BUILD"] + defs   # enables the STENCIL_DEBUG_* / STENCIL_1D_* env knobs
     objs = []
     for src in tuned:
