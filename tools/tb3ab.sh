@@ -2,7 +2,7 @@
 cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
 good=""
 for v in "$@"; do
-  if STENCIL_B200_LIB=tunelibs/lib_$v.so timeout 200 python -m pytest tests/test_gpu_tb3d.py -q -x > gpurun_out/tb3ab_$v.log 2>&1; then good="$good $v"; echo "$v tests ok"; else echo "$v tests FAILED"; tail -3 gpurun_out/tb3ab_$v.log; fi
+  if STENCIL_B200_LIB=tunelibs/lib_$v.so timeout 200 python -m pytest tests/test_gpu_tb3d.py -q -x ${TB3_TESTK:+-k "$TB3_TESTK"} > gpurun_out/tb3ab_$v.log 2>&1; then good="$good $v"; echo "$v tests ok"; else echo "$v tests FAILED"; tail -3 gpurun_out/tb3ab_$v.log; fi
 done
 for pass in a b; do
   for name in main $good; do
