@@ -80,9 +80,14 @@ struct Tb3Cfg {
 #define TB3_CHAIN_XLAST 1   // (measured: C4 K=4 624 vs 608, K=3 561 vs 535 GStencil/s)
 #endif
     static constexpr int PF = TB3_PF;                   // planes in flight ahead
+#ifndef TB3_RING_GLOBAL
+#define TB3_RING_GLOBAL 0
+#endif
     // TMA plane slots: the 2K - 1 planes behind the current one stay resident,
     // so the frozen ring cells of every level are re-read from shared memory
-    static constexpr int D = 2 * K + PF;
+    // (TB3_RING_GLOBAL: re-read from src in global memory; only the current
+    // plane and the PF planes in flight need a slot)
+    static constexpr int D = TB3_RING_GLOBAL ? PF + 1 : 2 * K + PF;
     static constexpr int PLANE = TX * TY;               // elements per slot
     static constexpr int NPO = K > 1 ? K - 1 : 1;       // published levels 1..K-1
     static constexpr int EDGE_ELEMS = NPO * 2 * NWY * 2 * TX;   // [level][parity][warp][top|bottom][TX]
@@ -135,7 +140,7 @@ __device__ __forceinline__ void tb3_iter(const Tb3Cta<T, K, NWY, VY>& cta, const
                                          T (&a)[K][VY][Tb3Cfg<T, K, NWY, VY>::VX],
                                          T (&b)[K][VY][Tb3Cfg<T, K, NWY, VY>::VX],
                                          T (&po)[Tb3Cfg<T, K, NWY, VY>::NPO][VY][Tb3Cfg<T, K, NWY, VY>::VX], int t,
-                                         int i, int slot, uint32_t phase, T* gdst, unsigned omask, unsigned rmask,
+                                         int i, int slot, uint32_t phase, T* gdst, const T* gsrc, unsigned omask, unsigned rmask,
                                          unsigned fmask, int z0, int z1) {
     using C = Tb3Cfg<T, K, NWY, VY>;
     constexpr int VX = C::VX;
@@ -189,15 +194,25 @@ __device__ __forceinline__ void tb3_iter(const Tb3Cta<T, K, NWY, VY>& cta, const
             }
         const int j = i - 2 * s + 1;   // the level-s plane completed now (loaded 2s - 1 iterations ago)
         // frozen ring cells: u0 from the slot of plane j (still resident: D >= 2K + PF)
+#if TB3_RING_GLOBAL
+        // (from src in global memory: u0 is frozen there; only border tiles and
+        // the first/last planes of a segment read it, as L2 hits)
+        // (j is clamped into the allocated planes: pipeline-fill iterations complete
+        // planes outside them whose values are never used)
+        const T* uj = gsrc + (long long)min(max(j, (int)-P.org_z), P.ext_z - 1 - (int)P.org_z) * P.pz;
+        const long long rs = P.py;   // row stride
+#else
         const T* uj = cta.ring + (slot >= 2 * s - 1 ? slot - (2 * s - 1) : slot - (2 * s - 1) + C::D) * C::PLANE +
                       warp * VY * C::TX + lane * VX;
+        constexpr long long rs = C::TX;
+#endif
         if constexpr (EDGE) {          // ring columns / rows
             if (rmask) {
 #pragma unroll
                 for (int r = 0; r < VY; ++r)
 #pragma unroll
                     for (int e = 0; e < VX; ++e)
-                        if ((rmask >> (r * VX + e)) & 1u) o[r][e] = uj[r * C::TX + e];
+                        if ((rmask >> (r * VX + e)) & 1u) o[r][e] = uj[r * rs + e];
             }
         }
         if constexpr (CHK) {           // ring planes
@@ -206,7 +221,7 @@ __device__ __forceinline__ void tb3_iter(const Tb3Cta<T, K, NWY, VY>& cta, const
                 for (int r = 0; r < VY; ++r)
 #pragma unroll
                     for (int e = 0; e < VX; ++e)
-                        if ((fmask >> (r * VX + e)) & 1u) o[r][e] = uj[r * C::TX + e];
+                        if ((fmask >> (r * VX + e)) & 1u) o[r][e] = uj[r * rs + e];
             }
         }
         if (s < K) {   // hand the level-s plane to stage s+1 (next iteration)
@@ -301,6 +316,7 @@ __device__ __forceinline__ void tb3_unit(Tb3Cta<T, K, NWY, VY>& cta, const T (&w
             for (int e = 0; e < VX; ++e) po[s][r][e] = T(0);
     const long long base = P.org_x + gx + (P.org_y + gy) * P.py + P.org_z * P.pz;   // patch origin, plane 0
     T* gdst = P.dst + base;
+    const T* gsrc = P.src + base;
     // steady iterations: the stored plane j_K = i - 2K + 1 lies in [z0, z1)
     // without peer rows, and no stage completes a ring plane (j_1 = i - 1 < nz)
     int t_lo = z0 - i_lo + 2 * K - 1;
@@ -313,7 +329,7 @@ __device__ __forceinline__ void tb3_unit(Tb3Cta<T, K, NWY, VY>& cta, const T (&w
     auto body = [&](auto chk_tag, int t) {
         constexpr bool CHK = decltype(chk_tag)::value;
         if (threadIdx.x == 0 && t + C::PF < nit) issue(t + C::PF, sc + C::PF < C::D ? sc + C::PF : sc + C::PF - C::D);
-        tb3_iter<T, K, NWY, VY, CHK, EDGE>(cta, w, a, b, po, t, i_lo + t, sc, ph, gdst, omask, rmask, fmask, z0, z1);
+        tb3_iter<T, K, NWY, VY, CHK, EDGE>(cta, w, a, b, po, t, i_lo + t, sc, ph, gdst, gsrc, omask, rmask, fmask, z0, z1);
         if (++sc == C::D) {
             sc = 0;
             ph ^= 1u;
