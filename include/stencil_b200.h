@@ -330,6 +330,22 @@ int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void *buf, int h
                           void *stream);
 
 /*
+ * Diagnostic: the per-sweep NCCL exchange of stencil_run_dist (the same
+ * grouped ncclSend/ncclRecv calls, counts, datatype and plane addresses) with
+ * THIS rank as both neighbours, so the transport can be exercised on a box
+ * with one GPU (a 1-rank communicator has no neighbours otherwise).  Within
+ * the group, sends and receives to one peer match in issue order: afterwards
+ * buf's lower ghost planes [-halo, 0) hold its planes [0, halo) and its upper
+ * ghost planes [n0, n0 + halo) hold its planes [n0 - halo, n0).  NCCL comms
+ * only (EINVAL for a peer comm, a slab thinner than halo, or a halo beyond the
+ * planes the rank's layout holds outside its slab: ghost planes, or the
+ * r-ring at a physical face, which this call overwrites); every rank that
+ * calls it exchanges with itself only (not collective).
+ */
+int stencil_halo_exchange_loopback(stencil_plan plan, stencil_comm comm, void *buf, int halo,
+                                   void *stream);
+
+/*
  * Failure detection.  Wait until `stream` has drained, polling
  * the NCCL communicator's asynchronous error (ncclCommGetAsyncError) every
  * 0.2 ms.  On an asynchronous NCCL error the communicator is aborted

@@ -60,6 +60,7 @@ SIGNATURES = {
     "stencil_fill_random_dist": (c_int, [c_vp, c_int, c_int, c_int, c_vp, c_u64, c_vp]),
     "stencil_run_dist": (c_int, [c_vp, c_vp, c_vp, c_vp, c_i64, c_int, c_int, c_int, c_vp, c_vp]),
     "stencil_halo_exchange": (c_int, [c_vp, c_vp, c_vp, c_int, c_vp]),
+    "stencil_halo_exchange_loopback": (c_int, [c_vp, c_vp, c_vp, c_int, c_vp]),
     "stencil_run_dist_emulated": (c_int, [c_vp, c_int, ctypes.POINTER(c_vp), ctypes.POINTER(c_vp), c_i64, c_int,
                                           c_int, c_int, ctypes.POINTER(c_vp), c_int, c_vp]),
     "stencil_comm_create_peer": (c_int, [ctypes.POINTER(c_vp), c_int, c_int, c_vp, c_vp]),

@@ -254,6 +254,10 @@ class Plan:
     def halo_exchange(self, comm: "Comm", buf, halo, stream=None):
         check(self._lib.stencil_halo_exchange(self._h, comm._h, _ptr(buf), int(halo), _stream(stream)))
 
+    def halo_exchange_loopback(self, comm: "Comm", buf, halo, stream=None):
+        """Diagnostic: the NCCL exchange with this rank as both neighbours (one-GPU boxes)."""
+        check(self._lib.stencil_halo_exchange_loopback(self._h, comm._h, _ptr(buf), int(halo), _stream(stream)))
+
     def run_dist_emulated(self, ins, outs, T, fold_m, halo, workspaces=None, stages=0, stream=None,
                           exchange="copies"):
         """All ranks in this process on one GPU; exchange = "copies" (the NCCL

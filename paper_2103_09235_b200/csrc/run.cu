@@ -923,7 +923,10 @@ static int nccl_async_check(stencil_comm_s* c) {
     return STENCIL_OK;
 }
 
-static int nccl_exchange(Plan* p, stencil_comm_s* c, const Layout3& L, void* buf, int64_t hx, cudaStream_t st) {
+// lo_peer / hi_peer: the ranks owning the planes below / above this slab (-1: a
+// physical face, no exchange on that side).
+static int nccl_exchange_with(Plan* p, stencil_comm_s* c, const Layout3& L, void* buf, int64_t hx, cudaStream_t st,
+                              int lo_peer, int hi_peer) {
     int rc = nccl_async_check(c);
     if (rc) return rc;
     NcclApi& a = nccl();
@@ -939,18 +942,39 @@ static int nccl_exchange(Plan* p, stencil_comm_s* c, const Layout3& L, void* buf
     auto chk = [&](ncclResult_t x, const char* w) {
         if (x != ncclSuccess && first == ncclSuccess) { first = x; what = w; }
     };
-    if (c->rank > 0) {
-        chk(a.Send(plane(0), cnt, dt, c->rank - 1, c->comm, st), "ncclSend(lower)");
-        chk(a.Recv(plane(-hx), cnt, dt, c->rank - 1, c->comm, st), "ncclRecv(lower)");
+    if (lo_peer >= 0) {
+        chk(a.Send(plane(0), cnt, dt, lo_peer, c->comm, st), "ncclSend(lower)");
+        chk(a.Recv(plane(-hx), cnt, dt, lo_peer, c->comm, st), "ncclRecv(lower)");
     }
-    if (c->rank < c->nranks - 1) {
-        chk(a.Send(plane(L.n[0] - hx), cnt, dt, c->rank + 1, c->comm, st), "ncclSend(upper)");
-        chk(a.Recv(plane(L.n[0]), cnt, dt, c->rank + 1, c->comm, st), "ncclRecv(upper)");
+    if (hi_peer >= 0) {
+        chk(a.Send(plane(L.n[0] - hx), cnt, dt, hi_peer, c->comm, st), "ncclSend(upper)");
+        chk(a.Recv(plane(L.n[0]), cnt, dt, hi_peer, c->comm, st), "ncclRecv(upper)");
     }
     r = a.GroupEnd();   // always close the group, even after a failed call
     if (first != ncclSuccess) return nccl_error(first, what);
     if (r != ncclSuccess) return nccl_error(r, "ncclGroupEnd");
     return STENCIL_OK;
+}
+
+static int nccl_exchange(Plan* p, stencil_comm_s* c, const Layout3& L, void* buf, int64_t hx, cudaStream_t st) {
+    return nccl_exchange_with(p, c, L, buf, hx, st, c->rank > 0 ? c->rank - 1 : -1,
+                              c->rank < c->nranks - 1 ? c->rank + 1 : -1);
+}
+
+int stencil_halo_exchange_loopback(stencil_plan plan, stencil_comm comm, void* buf, int halo, void* stream) {
+    Plan* p = reinterpret_cast<Plan*>(plan);
+    if (!p || !comm || !buf) return set_error(STENCIL_EINVAL, "NULL argument");
+    Layout3 L;
+    int rc = dist_layout_check(p, comm->rank, comm->nranks, halo, 1, &L);
+    if (rc) return rc;
+    if (comm->peer) return set_error(STENCIL_EINVAL, "loopback exchange needs an NCCL comm");
+    if (L.n[0] < halo) return set_error(STENCIL_EINVAL, "slab thinner than the halo");
+    if (halo > L.origin[0] || halo > L.ext[0] - L.origin[0] - L.n[0])
+        return set_error(STENCIL_EINVAL, "halo exceeds the planes this layout allocates outside the slab");
+    // the sweep's exchange with this rank as both neighbours: in the group the
+    // sends and receives to one peer match in issue order, so planes [0, halo)
+    // land in the lower ghost planes and planes [n0 - halo, n0) in the upper
+    return nccl_exchange_with(p, comm, L, buf, halo, (cudaStream_t)stream, comm->rank, comm->rank);
 }
 
 int stencil_halo_exchange(stencil_plan plan, stencil_comm comm, void* buf, int halo, void* stream) {

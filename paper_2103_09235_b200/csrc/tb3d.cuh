@@ -79,6 +79,10 @@ struct Tb3Cfg {
 #ifndef TB3_CHAIN_XLAST
 #define TB3_CHAIN_XLAST 1   // (measured: C4 K=4 624 vs 608, K=3 561 vs 535 GStencil/s)
 #endif
+#ifndef TB3_K2_CPS
+#define TB3_K2_CPS 2        // resident CTAs per SM at K = 2: 128 registers, 2 x 112 KB (measured: C4 K=2 569 vs 519 GStencil/s)
+#endif
+    static constexpr int CPS = K == 2 ? TB3_K2_CPS : 1;
     static constexpr int PF = TB3_PF;                   // planes in flight ahead
 #ifndef TB3_RING_GLOBAL
 #define TB3_RING_GLOBAL 0
@@ -343,7 +347,7 @@ __device__ __forceinline__ void tb3_unit(Tb3Cta<T, K, NWY, VY>& cta, const T (&w
 }
 
 template <typename T, int K, int NWY, int VY>
-__global__ void __launch_bounds__(32 * NWY, 1)
+__global__ void __launch_bounds__(32 * NWY, Tb3Cfg<T, K, NWY, VY>::CPS)
     tb3d_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Tb3Params<T> p) {
     using C = Tb3Cfg<T, K, NWY, VY>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -452,7 +456,7 @@ int tb3d_launch(Plan* p, const SweepCall& c) {
     const int ntx = (prm.nx + C::WOX - 1) / C::WOX, nty = (prm.ny + C::WOY - 1) / C::WOY;
     const int tiles = ntx * nty;
     const int Z = prm.z_hi - prm.z_lo;
-    const int grid_max = std::max(1, p->sm_count);   // one CTA per SM
+    const int grid_max = std::max(1, p->sm_count) * C::CPS;   // one CTA per SM (K = 2: CPS)
     // z-segments: the count with the least (waves x (segment + pipeline fill))
     int best = 1;
     double bcost = 1e300;

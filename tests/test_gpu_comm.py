@@ -57,6 +57,45 @@ def test_nccl_single_rank_run_dist(dims, shape, dtype, T, m):
     comm.close()
 
 
+@pytest.mark.parametrize("dims,shape,dtype,r", [((64, 300), "star", "f64", 1), ((64, 300), "box", "f32", 3),
+                                                ((24, 40, 72), "star", "f64", 2),
+                                                ((16, 33, 70), "box", "f32", 1)])
+def test_nccl_send_recv_loopback(dims, shape, dtype, r):
+    """Real ncclSend/ncclRecv through the library's per-sweep exchange (grouped
+    calls, counts, datatype, plane addresses) with rank 0 as both neighbours:
+    ghost planes [-halo, 0) <- planes [0, halo), [n0, n0+halo) <- [n0-halo, n0);
+    nothing else in the buffer changes."""
+    from paper_2103_09235_b200 import Plan
+    from paper_2103_09235_b200.api import Comm
+    offs = oracle.taps(len(dims), r, oracle.STAR if shape == "star" else oracle.BOX)
+    plan = Plan(dims, r, shape, synth.weights(len(offs), 1), dtype)
+    halo = r                                       # a 1-rank layout holds the r-ring outside the slab
+    comm = Comm(Comm.unique_id(), 0, 1)
+    with pytest.raises(Exception):
+        plan.halo_exchange_loopback(comm, plan.empty(), r + 1)
+    L = plan.layout_dist(0, 1, halo)
+    a = plan.empty(layout=L)
+    plan.fill_random_dist(0, 1, halo, a, 7)
+    torch.cuda.synchronize()
+    before = a.clone()
+    plan.halo_exchange_loopback(comm, a, halo)
+    comm.wait(timeout_ms=60000)
+    torch.cuda.synchronize()
+    n0 = dims[0]
+    pl = L.stride[0]                               # elements per axis-0 plane
+    o0 = L.origin[0]
+    fa, fb = a.view(-1), before.view(-1)
+    def planes(t, z0, z1):
+        return t[(o0 + z0) * pl:(o0 + z1) * pl]
+    assert torch.equal(planes(fa, -halo, 0), planes(fb, 0, halo))
+    assert torch.equal(planes(fa, n0, n0 + halo), planes(fb, n0 - halo, n0))
+    assert torch.equal(planes(fa, 0, n0), planes(fb, 0, n0))
+    assert torch.equal(fa[:(o0 - halo) * pl], fb[:(o0 - halo) * pl])
+    assert torch.equal(fa[(o0 + n0 + halo) * pl:], fb[(o0 + n0 + halo) * pl:])
+    assert not torch.equal(planes(fa, -halo, 0), planes(fb, -halo, 0))   # the exchange did move data
+    comm.close()
+
+
 def _peer_worker(rank, world, port, outdir, dims, shape, dtype, m, K):
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
