@@ -579,7 +579,7 @@ def run_ours(args):
     key = "%s/m%d/s%d" % (args.config, m, args.stages)
     var = plan.variant(m) if nd >= 2 and args.stages == 0 else None
     tb = m > 1 and ((var is not None and var[0] == 1 and var[1] == m) or args.stages == m) and (
-        nd == 2 or (nd == 3 and cfg["shape"] == "star" and cfg["dtype"] == "f64" and m <= 4))
+        nd == 2 or (nd == 3 and cfg["dtype"] == "f64" and (m <= 4 if cfg["shape"] == "star" else m == 2)))
     kernel_name = ("tb%dd_kernel (on-chip temporal block, %d steps per HBM round trip)" % (nd, m) if tb else
                    "onchip1d_kernel (fold_m=%d)" % m if nd == 1 else "sweep_kernel (main region, fold_m=%d)" % m)
     roof = {"bound": "alu" if alu_bound else "hbm",

@@ -3,6 +3,9 @@
 // registers over the tiles efficiently without reloading", §3.4; "time
 // loop fusion").  One launch applies K single steps of the
 // original 7 taps per HBM round trip, exactly up to the FIXED faces (no band).
+// The same block with BOX = true applies K = 2 single steps of the 27 taps of
+// the radius-1 box (3D27P, BASELINE fold_m = 2 for C5): the arriving plane adds
+// a 9-point in-plane sum to each of the three output planes in flight.
 //
 // B200 mapping:
 //  * A CTA is an overlapped TY x TX tile of the (y, x) plane streamed along z
@@ -59,6 +62,7 @@ struct Tb3Params {
     long long peer_dlo, peer_dhi;
     int peer_h, peer_lo_on, peer_hi_on;
     T w[7];                         // 3D7P taps in canonical order: z-, y-, x-, c, x+, y+, z+
+    T wb[27];                       // 3D27P: the dense 3x3x3 table, index ((dz+1)*3 + dy+1)*3 + dx+1
 };
 
 template <typename T, int K, int NWY, int VY>
@@ -82,7 +86,7 @@ struct Tb3Cfg {
 #ifndef TB3_K2_CPS
 #define TB3_K2_CPS 2        // resident CTAs per SM at K = 2: 128 registers, 2 x 112 KB (measured: C4 K=2 569 vs 519 GStencil/s)
 #endif
-    static constexpr int CPS = K == 2 ? TB3_K2_CPS : 1;
+    static constexpr int CPS = K == 2 ? TB3_K2_CPS : 1;   // (stars; the box block keeps one CTA per SM)
     static constexpr int PF = TB3_PF;                   // planes in flight ahead
 #ifndef TB3_RING_GLOBAL
 #define TB3_RING_GLOBAL 0
@@ -139,7 +143,7 @@ struct Tb3Cta {
 
 // The per-unit body is written as a free function so that the steady and the
 // checked iterations are two instantiations of one iteration template.
-template <typename T, int K, int NWY, int VY, bool CHK, bool EDGE>
+template <typename T, int K, int NWY, int VY, bool BOX, bool CHK, bool EDGE>
 __device__ __forceinline__ void tb3_iter(const Tb3Cta<T, K, NWY, VY>& cta, const T (&w)[7],
                                          T (&a)[K][VY][Tb3Cfg<T, K, NWY, VY>::VX],
                                          T (&b)[K][VY][Tb3Cfg<T, K, NWY, VY>::VX],
@@ -171,13 +175,65 @@ __device__ __forceinline__ void tb3_iter(const Tb3Cta<T, K, NWY, VY>& cta, const
             Tb3Cta<T, K, NWY, VY>::ldv(U, cta.edge_row(s - 1, par ^ 1, max(warp - 1, 0), 1) + lane * VX);
             Tb3Cta<T, K, NWY, VY>::ldv(Dn, cta.edge_row(s - 1, par ^ 1, min(warp + 1, NWY - 1), 0) + lane * VX);
         }
+        T o[VY][VX];
+        if constexpr (BOX) {
+            // 3D27P: the arriving plane v contributes a 9-point in-plane sum to three
+            // output planes: it completes plane z-1 (dz = +1 weights onto a), seeds plane
+            // z (dz = 0 onto b) and plane z+1 (dz = -1).  Rows q = 0 (U), 1..VY (v),
+            // VY+1 (Dn); their x-neighbours by warp shuffle.
+            T Lc[VY + 2], Rc[VY + 2];
+#pragma unroll
+            for (int q = 0; q < VY + 2; ++q) {
+                const T(&row)[VX] = q == 0 ? U : (q == VY + 1 ? Dn : v[q == 0 || q == VY + 1 ? 0 : q - 1]);
+                Lc[q] = __shfl_up_sync(0xffffffffu, row[VX - 1], 1);
+                Rc[q] = __shfl_down_sync(0xffffffffu, row[0], 1);
+            }
+            // tap-major order: the 3 VY VX accumulator chains advance together, so
+            // consecutive multiply-adds are independent (DFMA latency 8 cycles)
+            T sn[VY][VX];
+#pragma unroll
+            for (int r = 0; r < VY; ++r)
+#pragma unroll
+                for (int e = 0; e < VX; ++e) {
+                    o[r][e] = a[s - 1][r][e];
+                    a[s - 1][r][e] = b[s - 1][r][e];
+                }
+            // (the centre column and row first: the shuffled and shared-memory operands last)
+#pragma unroll
+            for (int iy = 0; iy < 3; ++iy)
+#pragma unroll
+                for (int ix = 0; ix < 3; ++ix) {
+                    const int dy = iy == 0 ? 0 : (iy == 1 ? -1 : 1), dx = ix == 0 ? 0 : (ix == 1 ? -1 : 1);
+                    const int k = (dy + 1) * 3 + dx + 1;
+                    // (weights as constant-bank / uniform-register operands: a DFMA then reads two
+                    // vector registers; with the 27 weights in vector registers, three reads per
+                    // DFMA, C5 K=2 measured 302 vs 347 GStencil/s)
+                    const T wp = P.wb[18 + k], wc = P.wb[9 + k], wm = P.wb[k];
+#pragma unroll
+                    for (int r = 0; r < VY; ++r) {
+                        const int q = r + 1 + dy;
+                        const T(&row)[VX] = q == 0 ? U : (q == VY + 1 ? Dn : v[q == 0 || q == VY + 1 ? 0 : q - 1]);
+#pragma unroll
+                        for (int e = 0; e < VX; ++e) {
+                            const int c = e + dx;
+                            const T x = c < 0 ? Lc[q] : (c >= VX ? Rc[q] : row[c < 0 || c >= VX ? 0 : c]);
+                            o[r][e] = fma(wp, x, o[r][e]);
+                            a[s - 1][r][e] = fma(wc, x, a[s - 1][r][e]);
+                            sn[r][e] = (iy == 0 && ix == 0) ? wm * x : fma(wm, x, sn[r][e]);
+                        }
+                    }
+                }
+#pragma unroll
+            for (int r = 0; r < VY; ++r)
+#pragma unroll
+                for (int e = 0; e < VX; ++e) b[s - 1][r][e] = sn[r][e];
+        } else {
         T L[VY], R[VY];
 #pragma unroll
         for (int r = 0; r < VY; ++r) {
             L[r] = __shfl_up_sync(0xffffffffu, v[r][VX - 1], 1);
             R[r] = __shfl_down_sync(0xffffffffu, v[r][0], 1);
         }
-        T o[VY][VX];
 #pragma unroll
         for (int r = 0; r < VY; ++r)
 #pragma unroll
@@ -196,6 +252,7 @@ __device__ __forceinline__ void tb3_iter(const Tb3Cta<T, K, NWY, VY>& cta, const
 #endif
                 b[s - 1][r][e] = w[0] * v[r][e];
             }
+        }
         const int j = i - 2 * s + 1;   // the level-s plane completed now (loaded 2s - 1 iterations ago)
         // frozen ring cells: u0 from the slot of plane j (still resident: D >= 2K + PF)
 #if TB3_RING_GLOBAL
@@ -269,7 +326,7 @@ __device__ __forceinline__ void tb3_iter(const Tb3Cta<T, K, NWY, VY>& cta, const
     __syncthreads();
 }
 
-template <typename T, int K, int NWY, int VY, bool EDGE>
+template <typename T, int K, int NWY, int VY, bool BOX, bool EDGE>
 __device__ __forceinline__ void tb3_unit(Tb3Cta<T, K, NWY, VY>& cta, const T (&w)[7], int x0, int y0, int z0,
                                          int z1) {
     using C = Tb3Cfg<T, K, NWY, VY>;
@@ -333,7 +390,7 @@ __device__ __forceinline__ void tb3_unit(Tb3Cta<T, K, NWY, VY>& cta, const T (&w
     auto body = [&](auto chk_tag, int t) {
         constexpr bool CHK = decltype(chk_tag)::value;
         if (threadIdx.x == 0 && t + C::PF < nit) issue(t + C::PF, sc + C::PF < C::D ? sc + C::PF : sc + C::PF - C::D);
-        tb3_iter<T, K, NWY, VY, CHK, EDGE>(cta, w, a, b, po, t, i_lo + t, sc, ph, gdst, gsrc, omask, rmask, fmask, z0, z1);
+        tb3_iter<T, K, NWY, VY, BOX, CHK, EDGE>(cta, w, a, b, po, t, i_lo + t, sc, ph, gdst, gsrc, omask, rmask, fmask, z0, z1);
         if (++sc == C::D) {
             sc = 0;
             ph ^= 1u;
@@ -346,8 +403,8 @@ __device__ __forceinline__ void tb3_unit(Tb3Cta<T, K, NWY, VY>& cta, const T (&w
     cta.phase = ph;
 }
 
-template <typename T, int K, int NWY, int VY>
-__global__ void __launch_bounds__(32 * NWY, Tb3Cfg<T, K, NWY, VY>::CPS)
+template <typename T, int K, int NWY, int VY, bool BOX>
+__global__ void __launch_bounds__(32 * NWY, BOX ? 1 : Tb3Cfg<T, K, NWY, VY>::CPS)
     tb3d_kernel(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ Tb3Params<T> p) {
     using C = Tb3Cfg<T, K, NWY, VY>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -403,15 +460,15 @@ __global__ void __launch_bounds__(32 * NWY, Tb3Cfg<T, K, NWY, VY>::CPS)
         const int z0 = p.z_lo + seg * p.seglen, z1 = min(z0 + p.seglen, p.z_hi);
         if (z0 >= z1) continue;
         const bool edge = x0 <= -1 || x0 + C::TX > p.nx || y0 <= -1 || y0 + C::TY > p.ny;
-        if (edge) tb3_unit<T, K, NWY, VY, true>(cta, w, x0, y0, z0, z1);
-        else tb3_unit<T, K, NWY, VY, false>(cta, w, x0, y0, z0, z1);
+        if (edge) tb3_unit<T, K, NWY, VY, BOX, true>(cta, w, x0, y0, z0, z1);
+        else tb3_unit<T, K, NWY, VY, BOX, false>(cta, w, x0, y0, z0, z1);
     }
 }
 
 // ------------------------------------------------------------------ host
 PFN_cuTensorMapEncodeTiled_v12000 tb_encode_fn();
 
-template <typename T, int K, int NWY, int VY>
+template <typename T, int K, int NWY, int VY, bool BOX = false>
 int tb3d_launch(Plan* p, const SweepCall& c) {
     using C = Tb3Cfg<T, K, NWY, VY>;
     const Layout3& L = *c.L;
@@ -443,6 +500,7 @@ int tb3d_launch(Plan* p, const SweepCall& c) {
     // the 7 star entries of the dense table, index ((dz+1)*3 + dy+1)*3 + dx+1, canonical order
     const int idx[7] = {4, 10, 12, 13, 14, 16, 22};
     for (int k = 0; k < 7; ++k) prm.w[k] = static_cast<T>((*c.coef)[idx[k]]);
+    for (int k = 0; k < 27; ++k) prm.wb[k] = static_cast<T>((*c.coef)[k]);
     if (c.peer_h > 0) {
         const long long plane = (long long)L.n[0] * L.stride[0] * (long long)sizeof(T);
         prm.peer_h = c.peer_h;
@@ -456,7 +514,7 @@ int tb3d_launch(Plan* p, const SweepCall& c) {
     const int ntx = (prm.nx + C::WOX - 1) / C::WOX, nty = (prm.ny + C::WOY - 1) / C::WOY;
     const int tiles = ntx * nty;
     const int Z = prm.z_hi - prm.z_lo;
-    const int grid_max = std::max(1, p->sm_count) * C::CPS;   // one CTA per SM (K = 2: CPS)
+    const int grid_max = std::max(1, p->sm_count) * (BOX ? 1 : C::CPS);   // one CTA per SM (star K = 2: CPS)
     // z-segments: the count with the least (waves x (segment + pipeline fill))
     int best = 1;
     double bcost = 1e300;
@@ -492,13 +550,13 @@ int tb3d_launch(Plan* p, const SweepCall& c) {
         cudaGetDevice(&dev);
         std::lock_guard<std::mutex> g(mu);
         if (dev >= 0 && dev < 64 && !done[dev]) {
-            cudaError_t e = cudaFuncSetAttribute(tb3d_kernel<T, K, NWY, VY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+            cudaError_t e = cudaFuncSetAttribute(tb3d_kernel<T, K, NWY, VY, BOX>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)C::SMEM);
             if (e != cudaSuccess) return cuda_error(e, "cudaFuncSetAttribute(tb3d)");
             done[dev] = true;
         }
     }
-    tb3d_kernel<T, K, NWY, VY><<<grid, C::NT, C::SMEM, (cudaStream_t)c.stream>>>(map, prm);
+    tb3d_kernel<T, K, NWY, VY, BOX><<<grid, C::NT, C::SMEM, (cudaStream_t)c.stream>>>(map, prm);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return cuda_error(e, "tb3d_kernel launch");
     return 1;

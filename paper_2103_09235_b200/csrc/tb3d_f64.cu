@@ -13,6 +13,10 @@ namespace sb {
 #endif
 
 Tb3LaunchFn pick_tb3d_f64(int shape, int K) {
+    if (shape == STENCIL_BOX) {   // 3D27P: FMA-bound, K = 2 (K = 3 loses more to the halo than it saves)
+        if (K == 2) return tb3d_launch<double, 2, TB3_NWY, TB3_VY, true>;
+        return nullptr;
+    }
     if (shape != STENCIL_STAR) return nullptr;
     switch (K) {
         case 2: return tb3d_launch<double, 2, TB3_NWY, TB3_VY>;

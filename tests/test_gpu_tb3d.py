@@ -152,3 +152,100 @@ def test_tb3d_fullsize_c4():
     expect = field[inner] + T * sum(c * m for c, m in zip(coef, mu))
     err = float((plan.frame_view(b)[inner] - expect).abs().max())
     assert err <= TOL * 4.4, err
+
+
+# ------------------------------------------------------------------ 3D27P box, K = 2
+def _run_box(dims, T, u0=None, w=None, K=2):
+    from paper_2103_09235_b200 import Plan
+    offs = oracle.taps(3, 1, oracle.BOX)
+    if w is None:
+        w = synth.weights(len(offs), 1)
+    if u0 is None:
+        u0 = synth.u0_frame(dims, 1, 2)
+    ref = oracle.run(dims, 1, offs, w, u0, T)
+    plan = Plan(dims, 1, "box", w, "f64")
+    assert tuple(plan.variant(K))[:2] == (1, K)   # the stepwise evaluation: K single steps per round trip
+    a = plan.from_frame(u0)
+    b, ws = plan.empty(), plan.empty()
+    plan.run(a, b, T, K, workspace=ws, stages=K)
+    torch.cuda.synchronize()
+    return plan.frame_view(b).cpu().double().numpy(), ref, u0
+
+
+@pytest.mark.parametrize("T", [2, 5, 8])
+@pytest.mark.parametrize("dims", [(20, 33, 90), (37, 70, 150), (9, 5, 61), (3, 130, 20), (1, 1, 1), (64, 49, 57)])
+def test_tb3d_box_parity(T, dims):
+    got, ref, u0 = _run_box(dims, T)
+    err = float(np.max(np.abs(got - ref)))
+    assert err <= TOL * float(np.max(np.abs(u0))), err
+
+
+@pytest.mark.parametrize("dims,T", [((24, 40, 100), 6), ((8, 9, 10), 4), ((2, 66, 3), 4)])
+def test_tb3d_box_dyadic_bitwise(dims, T):
+    """Asymmetric dyadic weights: any transposed or mirrored tap of the 27 changes the bits."""
+    w = synth.dyadic_weights(27, seed=5, denom_bits=5)   # k/32: exact for 8 + 5T <= 53 bits
+    u0 = synth.dyadic_field(tuple(n + 2 for n in dims), seed=6)
+    got, ref, _ = _run_box(dims, T, u0=u0, w=w)
+    assert np.array_equal(got, ref)
+
+
+@pytest.mark.parametrize("exchange", ["copies", "peer"])
+@pytest.mark.parametrize("dims,G,T", [((48, 40, 100), 4, 9), ((16, 20, 30), 2, 5)])
+def test_tb3d_box_dist_emulated_bitwise(exchange, dims, G, T):
+    from paper_2103_09235_b200 import Plan
+    K = 2
+    plan = Plan(dims, 1, "box", synth.weights(27, 1), "f64")
+    a, b, ws = plan.empty(), plan.empty(), plan.empty()
+    plan.fill_random(a, 2)
+    plan.run(a, b, T, K, workspace=ws, stages=K)
+    single = plan.interior_view(b)
+    ins, outs, wss, Ls = [], [], [], []
+    for g in range(G):
+        L = plan.layout_dist(g, G, K)
+        Ls.append(L)
+        t = plan.empty(layout=L)
+        plan.fill_random_dist(g, G, K, t, 2)
+        ins.append(t)
+        outs.append(plan.empty(layout=L))
+        wss.append(plan.empty(layout=L))
+    plan.run_dist_emulated(ins, outs, T, K, K, wss, stages=K, exchange=exchange)
+    torch.cuda.synchronize()
+    per = dims[0] // G
+    for g in range(G):
+        assert torch.equal(plan.interior_view(outs[g], Ls[g]), single[g * per:(g + 1) * per]), g
+
+
+def test_tb3d_box_no_writes_outside():
+    from paper_2103_09235_b200 import Plan
+    dims, K = (20, 40, 100), 2
+    plan = Plan(dims, 1, "box", synth.weights(27, 1), "f64")
+    L = plan.layout
+    big, (a, b, ws), g, per = _carve(plan, L, 3)
+    plan.frame_view(a).copy_(torch.from_numpy(synth.u0_frame(dims, 1, 2)).to(plan.torch_dtype))
+    a_before = a.clone()
+    plan.run(a, b, 2 * K + 1, K, workspace=ws, stages=K)
+    torch.cuda.synchronize()
+    assert _guards_ok(big, g, per, 3)
+    assert torch.equal(a, a_before)
+
+
+def test_tb3d_box_fullsize_c5():
+    """C5 (768 x 768 x 384 fp64 3D27P, T = 100) at K = 2 (BASELINE fold_m = 2): cone-exact
+    samples at faces, edges, corners and tile seams."""
+    from paper_2103_09235_b200 import Plan
+    dims, T, K = (384, 768, 768), 100, 2
+    offs = oracle.taps(3, 1, oracle.BOX)
+    w = synth.weights(len(offs), 1)
+    plan = Plan(dims, 1, "box", w, "f64")
+    a, b, ws = plan.empty(), plan.empty(), plan.empty()
+    plan.fill_random(a, 2)
+    plan.run(a, b, T, K, workspace=ws, stages=K)
+    torch.cuda.synchronize()
+    inter = plan.interior_view(b)
+    z, y, x = dims
+    samples = [((0, 0, 0), (2, 2, 2)), ((z - 2, y - 2, x - 2), (z, y, x)), ((z // 2, 0, x - 2), (z // 2 + 1, 2, x)),
+               ((z // 2, 27, 59), (z // 2 + 1, 29, 61)), ((z - 1, 55, 119), (z, 57, 121))]   # 60 x 28 outputs per tile
+    for lo, hi in samples:
+        r = oracle.run_window(dims, 1, offs, w, T, lo, hi, lambda l, h: synth.u0_block(dims, 1, l, h, 2))
+        got = inter[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]].cpu().double().numpy()
+        assert float(np.max(np.abs(got - r))) <= TOL, (lo, hi)
