@@ -56,7 +56,7 @@ CONFIGS = {
     "c4": dict(name="3D7P star fp64 512^3 T=100", dims=(512, 512, 512), shape="star", dtype="f64", T=100,
                ms=(1, 2, 3, 4), best_m=4),
     "c5": dict(name="3D27P box fp64 768x768x384 T=100", dims=(384, 768, 768), shape="box", dtype="f64", T=100,
-               ms=(1, 2), best_m=1),
+               ms=(1, 2), best_m=2),
     # not a BASELINE config: C3's domain with the UNIFORM 2D9P weights of the paper's
     # worked example -- lambda^(m) has rank 1, so the plan evaluates it
     # through one counterpart (NEXT-3): 2*(2m+1) FMAs per point instead of (2m+1)^2

@@ -311,6 +311,8 @@ int auto_fold(Plan* p) {
     }
     if (p->ndim == 3 && p->r == 1) {
         if (p->shape == STENCIL_STAR && p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 4)) return 4;   // tb3d
+        // 27-point box: the K = 2 temporal block (tb3d, BOX) -- C5 378 vs 355-368 GStencil/s for m = 1
+        if (p->shape == STENCIL_BOX && p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 2)) return 2;
         return p->shape == STENCIL_STAR ? 2 : 1;
     }
     return 1;

@@ -226,4 +226,7 @@ def test_auto_fold_table():
     assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1), dtype="f32").auto_fold() == 2
     s3 = Plan((16, 16, 16), 1, "star", synth.weights(7, 1))
     assert s3.variant(2) == (2, 1, 0) and s3.variant(3) == (1, 3, 0) and s3.variant(4) == (1, 4, 0)
-    assert Plan((16, 16, 16), 1, "box", synth.weights(27, 1)).auto_fold() == 1
+    b3 = Plan((16, 16, 16), 1, "box", synth.weights(27, 1))
+    assert b3.auto_fold() == 2 and b3.variant(2) == (1, 2, 0)                             # temporal block (tb3d box)
+    assert Plan((16, 16, 16), 1, "box", synth.weights(27, 1), dtype="f32").auto_fold() == 1
+    assert Plan((16, 16, 16), 1, "box", synth.weights(27, 1), boundary="periodic").auto_fold() == 1

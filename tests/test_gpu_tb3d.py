@@ -244,7 +244,8 @@ def test_tb3d_box_fullsize_c5():
     inter = plan.interior_view(b)
     z, y, x = dims
     samples = [((0, 0, 0), (2, 2, 2)), ((z - 2, y - 2, x - 2), (z, y, x)), ((z // 2, 0, x - 2), (z // 2 + 1, 2, x)),
-               ((z // 2, 27, 59), (z // 2 + 1, 29, 61)), ((z - 1, 55, 119), (z, 57, 121))]   # 60 x 28 outputs per tile
+               ((z // 2, 51, 59), (z // 2 + 1, 53, 61)), ((z - 1, 103, 119), (z, 105, 121)),   # 60 x 52 outputs per tile
+               ((127, 727, 719), (129, 729, 721))]                                            # a z-segment seam, last tile row
     for lo, hi in samples:
         r = oracle.run_window(dims, 1, offs, w, T, lo, hi, lambda l, h: synth.u0_block(dims, 1, l, h, 2))
         got = inter[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]].cpu().double().numpy()
