@@ -291,6 +291,8 @@ def quick_measure(key, rank, world, dev, exchange, steps=5):
             e0.record(stream)
             step(m)
             e1.record(stream)
+            if comm is not None and exchange != "peer":
+                comm.wait(stream, timeout_ms=300000)   # NCCL async-error polling + timeout instead of a hang
             torch.cuda.synchronize()
             tot += e0.elapsed_time(e1)
         if world > 1:
@@ -409,6 +411,13 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
+    def drain():
+        # N > 1: wait through the library (polls the NCCL async error, aborts the
+        # communicator and raises after 5 min instead of hanging on a dead peer)
+        if comm is not None and args.exchange != "peer":
+            comm.wait(stream, timeout_ms=300000)
+        torch.cuda.synchronize()
+
     def allmax(x):
         if world == 1:
             return x
@@ -424,7 +433,7 @@ def run_ours(args):
         for _ in range(n):
             step(m, stages)
         e1.record(stream)
-        torch.cuda.synchronize()
+        drain()
         barrier()
         return allmax(e0.elapsed_time(e1) / n)
 
