@@ -167,10 +167,12 @@ int stencil_plan_set_counterparts(stencil_plan plan, int enable);
 /*
  * fold_m = 0 in stencil_run / stencil_run_ex / stencil_run_host /
  * stencil_run_dist means "auto": this fold, chosen per family from the B200
- * measurements: 1D 2; 2D FIXED radius 1: 8 (the on-chip
- * temporal block of 8 single steps per HBM round trip), or 4 when
- * lambda^(4) has a counterpart decomposition of rank <= 2; 2D PERIODIC: star
- * 3, box 2; 3D star 2; 3D box 1; radius > 1: 1.  Errors: EINVAL (NULL).
+ * measurements: 1D 2; 2D FIXED radius 1: 6 for fp64 stars
+ * and 8 otherwise (the on-chip temporal block: that many single steps per HBM
+ * round trip), or 4 when lambda^(4) has a counterpart decomposition of rank
+ * <= 2; 2D PERIODIC: star 3, box 2; 3D FIXED radius-1 fp64: star 4, box 2 (the
+ * 3D temporal block); other 3D stars 2, other 3D boxes 1; radius > 1: 1.
+ * Errors: EINVAL (NULL).
  */
 int stencil_plan_auto_fold(stencil_plan plan, int *fold_m);
 
