@@ -369,6 +369,11 @@ def run_ours(args):
     from paper_2103_09235_b200.dist import make_comm, make_peer_comm
 
     rank, world, local = env_int("RANK", 0), env_int("WORLD_SIZE", 1), env_int("LOCAL_RANK", 0)
+    if not torch.cuda.is_available() or local >= torch.cuda.device_count():
+        # no CPU fallback: say so in one line instead of a CUDA traceback per rank
+        sys.stderr.write("bench.py: rank %d needs cuda:%d but %d GPU(s) are visible\n"
+                         % (rank, local, torch.cuda.device_count() if torch.cuda.is_available() else 0))
+        return 2
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
