@@ -16,7 +16,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libstencil_b200.so")
 BUILD = os.path.join(ROOT, "build", "obj")
-SOURCES = ["tb2d_f64.cu", "tb3d_f64.cu", "tb2d_f32.cu", "onchip1d_wide.cu", "sweep_r2.cu", "sweep_2d.cu", "onchip1d_narrow.cu", "sweep_3d.cu", "sweep_cp.cu", "plan.cpp", "sweep.cu", "aux.cu", "run.cu"]
+SOURCES = ["tb2d_f64.cu", "tb3d_f64.cu", "tb2d_f32.cu", "tb3d_f32.cu", "onchip1d_wide.cu", "sweep_r2.cu", "sweep_2d.cu", "onchip1d_narrow.cu", "sweep_3d.cu", "sweep_cp.cu", "plan.cpp", "sweep.cu", "aux.cu", "run.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-std=c++20", "-O3", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",

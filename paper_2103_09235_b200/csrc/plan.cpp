@@ -185,8 +185,9 @@ Variant choose_variant(Plan* p, int m) {
     // 3D radius-1 fp64 FIXED stars: the CTA-tile temporal block (tb3d.cuh, m single steps
     // per HBM round trip) beats one folded pass from m = 3 on -- measured on B200 (DESIGN.md
     // §5.8: C4 m=4 624 vs the folded m=2 571 GStencil/s; K=2 520)
+    // (fp32 stars: from m = 4 on -- 512^3: K = 4 983 vs 940 for the folded m = 2 pass, K = 3 905)
     if (p->ndim == 3 && p->r == 1 && p->boundary == STENCIL_BC_FIXED && p->shape == STENCIL_STAR &&
-        tb_supported(p, 1, m) && m >= 3)
+        tb_supported(p, 1, m) && m >= (p->dtype == STENCIL_F64 ? 3 : 4))
         return {1, m};
     if (full <= 64) return {m, 1};
     Variant best = {m, 1};
@@ -310,9 +311,12 @@ int auto_fold(Plan* p) {
         return 2;
     }
     if (p->ndim == 3 && p->r == 1) {
-        if (p->shape == STENCIL_STAR && p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 4)) return 4;   // tb3d
+        if (p->shape == STENCIL_STAR && p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 4))
+            return 4;   // tb3d (fp64 C4: 635 vs 541-588 for m = 2; fp32 512^3: 983 vs 940)
         // 27-point box: the K = 2 temporal block (tb3d, BOX) -- C5 378 vs 355-368 GStencil/s for m = 1
-        if (p->shape == STENCIL_BOX && p->boundary == STENCIL_BC_FIXED && tb_supported(p, 1, 2)) return 2;
+        if (p->shape == STENCIL_BOX && p->boundary == STENCIL_BC_FIXED && p->dtype == STENCIL_F64 &&
+            tb_supported(p, 1, 2))
+            return 2;
         return p->shape == STENCIL_STAR ? 2 : 1;
     }
     return 1;

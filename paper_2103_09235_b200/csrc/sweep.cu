@@ -16,11 +16,11 @@ static LaunchFn pick(int dtype, int nd, int shape, int r, int q, int s) {
 
 // The on-chip stepwise block (q = 1, stages = m) of a 2D radius-1 FIXED plan
 // runs in the warp-tile temporal-blocking kernel (tb2d.cuh); that of a 3D
-// radius-1 fp64 star in the CTA-tile temporal block (tb3d.cuh).
+// radius-1 star or 27-point box in the CTA-tile temporal block (tb3d.cuh).
 static TbLaunchFn pick_tb(const Plan* p, int q, int s, int rank, bool wrap) {
     if (rank != 0 || q != 1 || s < 2 || p->r != 1 || wrap) return nullptr;
     if (p->ndim == 2) return p->dtype == STENCIL_F64 ? pick_tb2d_f64(p->shape, s) : pick_tb2d_f32(p->shape, s);
-    if (p->ndim == 3 && p->dtype == STENCIL_F64) return pick_tb3d_f64(p->shape, s);
+    if (p->ndim == 3) return p->dtype == STENCIL_F64 ? pick_tb3d_f64(p->shape, s) : pick_tb3d_f32(p->shape, s);
     return nullptr;
 }
 

@@ -86,7 +86,7 @@ struct Tb3Cfg {
 #ifndef TB3_K2_CPS
 #define TB3_K2_CPS 2        // resident CTAs per SM at K = 2: 128 registers, 2 x 112 KB (measured: C4 K=2 569 vs 519 GStencil/s)
 #endif
-    static constexpr int CPS = K == 2 ? TB3_K2_CPS : 1;   // (stars; the box block keeps one CTA per SM)
+    static constexpr int CPS = (K == 2 && sizeof(T) == 8) ? TB3_K2_CPS : 1;   // (fp64 stars; the box block keeps one CTA per SM)
     static constexpr int PF = TB3_PF;                   // planes in flight ahead
 #ifndef TB3_RING_GLOBAL
 #define TB3_RING_GLOBAL 0
@@ -564,5 +564,6 @@ int tb3d_launch(Plan* p, const SweepCall& c) {
 
 using Tb3LaunchFn = int (*)(Plan*, const SweepCall&);
 Tb3LaunchFn pick_tb3d_f64(int shape, int K);
+Tb3LaunchFn pick_tb3d_f32(int shape, int K);
 
 }  // namespace sb

@@ -223,7 +223,9 @@ def test_auto_fold_table():
     assert st.variant(3) == (3, 1, 0) and st.variant(4) == (1, 4, 0) and st.variant(8) == (1, 8, 0)
     assert bx.variant(2) == (2, 1, 0) and bx.variant(3) == (1, 3, 0)
     assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1)).auto_fold() == 4          # temporal block (tb3d)
-    assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1), dtype="f32").auto_fold() == 2
+    f3 = Plan((16, 16, 16), 1, "star", synth.weights(7, 1), dtype="f32")
+    assert f3.auto_fold() == 4 and f3.variant(4) == (1, 4, 0) and f3.variant(3) == (3, 1, 0)   # tb3d fp32 from m = 4
+    assert Plan((16, 16, 16), 1, "star", synth.weights(7, 1), dtype="f32", boundary="periodic").auto_fold() == 2
     s3 = Plan((16, 16, 16), 1, "star", synth.weights(7, 1))
     assert s3.variant(2) == (2, 1, 0) and s3.variant(3) == (1, 3, 0) and s3.variant(4) == (1, 4, 0)
     b3 = Plan((16, 16, 16), 1, "box", synth.weights(27, 1))

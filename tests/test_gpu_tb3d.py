@@ -250,3 +250,48 @@ def test_tb3d_box_fullsize_c5():
         r = oracle.run_window(dims, 1, offs, w, T, lo, hi, lambda l, h: synth.u0_block(dims, 1, l, h, 2))
         got = inter[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]].cpu().double().numpy()
         assert float(np.max(np.abs(got - r))) <= TOL, (lo, hi)
+
+
+# ------------------------------------------------------------------ fp32 (star K = 2..4, box K = 2)
+@pytest.mark.parametrize("shape,K", [("star", 2), ("star", 3), ("star", 4), ("box", 2)])
+@pytest.mark.parametrize("dims", [(20, 33, 90), (37, 70, 300), (9, 5, 61), (1, 1, 1), (64, 49, 257)])
+def test_tb3d_f32_parity(shape, K, dims):
+    from paper_2103_09235_b200 import Plan
+    offs = oracle.taps(3, 1, oracle.STAR if shape == "star" else oracle.BOX)
+    w = synth.weights(len(offs), 1)
+    u0 = synth.u0_frame(dims, 1, 2)
+    T = 2 * K + 1
+    ref = oracle.run(dims, 1, offs, w, u0, T)
+    plan = Plan(dims, 1, shape, w, "f32")
+    a = plan.from_frame(u0)
+    b, ws = plan.empty(), plan.empty()
+    plan.run(a, b, T, K, workspace=ws, stages=K)
+    torch.cuda.synchronize()
+    got = plan.frame_view(b).cpu().double().numpy()
+    err = float(np.max(np.abs(got - ref)))
+    assert err <= 2e-5 * float(np.max(np.abs(u0))), err
+
+
+@pytest.mark.parametrize("shape,K,G", [("star", 4, 4), ("box", 2, 2)])
+def test_tb3d_f32_dist_emulated_bitwise(shape, K, G):
+    from paper_2103_09235_b200 import Plan
+    dims, T = (48, 40, 200), 2 * K + 1
+    plan = Plan(dims, 1, shape, synth.weights(7 if shape == "star" else 27, 1), "f32")
+    a, b, ws = plan.empty(), plan.empty(), plan.empty()
+    plan.fill_random(a, 2)
+    plan.run(a, b, T, K, workspace=ws, stages=K)
+    single = plan.interior_view(b)
+    ins, outs, wss, Ls = [], [], [], []
+    for g in range(G):
+        L = plan.layout_dist(g, G, K)
+        Ls.append(L)
+        t = plan.empty(layout=L)
+        plan.fill_random_dist(g, G, K, t, 2)
+        ins.append(t)
+        outs.append(plan.empty(layout=L))
+        wss.append(plan.empty(layout=L))
+    plan.run_dist_emulated(ins, outs, T, K, K, wss, stages=K, exchange="peer")
+    torch.cuda.synchronize()
+    per = dims[0] // G
+    for g in range(G):
+        assert torch.equal(plan.interior_view(outs[g], Ls[g]), single[g * per:(g + 1) * per]), g

@@ -20,8 +20,8 @@ def main():
     B.build()
     out = os.path.join(ROOT, "tunelibs")
     os.makedirs(out, exist_ok=True)
-    src = "tb3d_f64.cu"
-    obj = os.path.join(out, "tb3d_f64_%s.o" % name)
+    src = os.environ.get("TB3_SRC", "tb3d_f64.cu")   # (TB3_SRC=tb3d_f32.cu for the fp32 unit)
+    obj = os.path.join(out, "%s_%s.o" % (src[:-3], name))
     cmd = [B.NVCC] + B.ARCH + B.FLAGS + defs + ["-Xptxas", "-v", "-c", os.path.join(B.CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     open(os.path.join(out, name + ".ptxas"), "w").write(r.stderr)
